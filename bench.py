@@ -1,0 +1,294 @@
+#!/usr/bin/env python
+"""Benchmark: FP64 ADI cell-updates/s (incl. Picard iterations) and % of the
+HBM roofline (BASELINE.json metric) on configs[3] -- the large grid
+Nr=8192 x Nz=16384, fixed dt 1e-5 -- one JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--mode fast|exact]
+  python bench.py --impl reference   # the reference's own CPU AdiStepper
+
+A "step" is one accepted ADI time step (AdiStepper::step, solver.cpp:356-373)
+of the whole grid. Cell-updates count every half-step attempt's active cells x
+Picard iterations. Multi-GPU (torchrun): each rank advances its
+own replica of the grid (the z-slab partition is not wired into the bench
+yet), so the job is weak-scaled; time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}  # B200_PROFILING.md fallback
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return PEAKS_FALLBACK["hbm_gbs"], "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.samples, self._stop = index, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 3 + k and s[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_sample_case(case, nz_sample: int):
+    """A z-truncated slice of the workload (same radial lines, materials, tau)."""
+    from paper_1912_03744_b200 import configs
+    return configs.scaled(case, case.gridspec.radial_divisions, nz_sample,
+                          name=case.name + f"-z{nz_sample}")
+
+
+def run_reference_cpu(case, steps: int, warmup: int, nz_sample: int, workers: int):
+    """The reference's own AdiStepper (oracle/_ref, compiled from its sources)
+    on a LinePool of `workers` threads: `warmup` untimed + `steps` timed step()
+    calls (bench.cpp:12-25 semantics) on a z-truncated sample."""
+    import numpy as np
+    from oracle.oracle import RefStepper, ref_available, PortStepper
+    from paper_1912_03744_b200.solver import make_field
+    sample = cpu_sample_case(case, nz_sample)
+    g = sample.grid()
+    if ref_available():
+        stepper, kind = RefStepper(sample, workers=workers), "reference"
+    else:
+        stepper, kind, workers = PortStepper(sample), "port", 1
+    f = make_field(g, sample.solver.T0)
+    t = 0.0
+    if warmup:
+        t, _, _ = stepper.run(f, t, warmup)
+    t0 = time.perf_counter()
+    t_end, stats, _ = stepper.run(f, t, steps)
+    dt = time.perf_counter() - t0
+    return {"value": stats["cell_updates"] / dt, "unit": "cell-updates/s", "cores": workers,
+            "kind": kind, "seconds": dt,
+            "sample": f"{g.nr()}x{g.nz()} z-slice of {case.name} (same radial lines, materials, "
+                      f"tau), {warmup} warm-up + {steps} timed step() calls, "
+                      f"{stats['cell_updates']:.3e} cell-updates"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default=os.environ.get("PCGPU_BENCH_MODE", "exact"),
+                    choices=["exact", "fast"])
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--cpu-nz", type=int, default=512, help="z-slice of the CPU sample")
+    ap.add_argument("--cpu-steps", type=int, default=1)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+
+    from paper_1912_03744_b200 import configs
+    case = configs.CONFIGS[args.config]()
+    grid_desc = {"workload": f"{case.name}: Nr={case.grid().nr()} x Nz={case.grid().nz()} FP64, "
+                             f"fixed dt {case.timing.t_src / case.solver.tau_source_divisor:g} s, "
+                             "4-layer cryogenic cell, power-law tables (SURVEY 8.0)"}
+    metric = "FP64 ADI cell-updates/s (incl. Picard iters)"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        workers = os.cpu_count() or 1
+        r = run_reference_cpu(case, max(1, args.steps // 10 or 1), min(args.warmup, 1),
+                              args.cpu_nz, workers)
+        line = {"impl": "reference", "metric": metric, "value": r["value"],
+                "unit": "cell-updates/s", "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "higher_is_better": True, "dtype": "f64",
+                "data": "synthetic", "config": dict(grid_desc, parallelism="cpu LinePool"),
+                "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": r["value"], "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import numpy as np
+    import torch
+
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        pg = dist
+
+    g = case.grid()
+    nr, nz = g.nr(), g.nz()
+    active = g.active_cells()
+    stepper = gpu_stepper_for(case, args.mode, local)
+    field = torch.full((nz, nr), case.solver.T0, dtype=torch.float64, device=f"cuda:{local}").t()
+    t = 0.0
+    # warm-up steps (untimed)
+    t, _, _ = stepper.run(field, t, args.warmup)
+    torch.cuda.synchronize()
+    stream = torch.cuda.ExternalStream(stepper.stream(), device=f"cuda:{local}")
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    launches0 = stepper.launch_count()
+    stepper.enable_kernel_timing(True)
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        t_end, stats, _ = stepper.run(field, t, args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = stepper.launch_count() - launches0
+    kt = stepper.kernel_timing()
+    stepper.enable_kernel_timing(False)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    if pg:
+        pg.all_reduce(ms_t, op=pg.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    updates = stats["cell_updates"] * world
+    value = updates / (ms_max / 1e3)
+
+    # Roofline of the dominant kernel: per-launch algorithmic bytes
+    # (active cells x 32 B per cell-update) / mean launch time.
+    peak, peak_kind = load_peaks()
+    sweeps = {"radial": (kt["radial_ms"], kt["radial_launches"]),
+              "axial": (kt["axial_ms"], kt["axial_launches"])}
+    dom = max(sweeps, key=lambda k: sweeps[k][0])
+    dom_ms, dom_n = sweeps[dom]
+    per_launch_bytes = active * 32.0
+    achieved = per_launch_bytes / (dom_ms / max(dom_n, 1) / 1e3) / 1e9 if dom_n else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(f"{args.mode}:{dom}")
+
+    # e2e through the reference-facing C-ABI with HOST buffers: pcgpu_step_host
+    # copies the field H2D, steps, copies D2H every step.
+    e2e = None
+    if not args.no_e2e:
+        host = np.asfortranarray(field.t().contiguous().cpu().numpy().T)
+        host_pinned = torch.from_numpy(np.ascontiguousarray(host.T)).pin_memory()
+        hp = host_pinned.numpy().T  # (nr, nz) F-ordered view of pinned memory
+        n_e2e = max(1, min(args.steps, 3))
+        upd = 0.0
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        te = t_end
+        for _ in range(n_e2e):
+            r = stepper.step(hp, te)
+            te += r.tau_used
+            upd += active * (r.radial.iterations + r.axial.iterations)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=f"cuda:{local}")
+        if pg:
+            pg.all_reduce(e_ms, op=pg.ReduceOp.MAX)
+        e2e = {"value": upd * world / (float(e_ms.item()) / 1e3), "unit": "cell-updates/s",
+               "h2d_bytes_per_step": nr * nz * 8, "d2h_bytes_per_step": nr * nz * 8,
+               "steps": n_e2e, "api": "pcgpu_step_host (C-ABI, host field)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = run_reference_cpu(case, args.cpu_steps, 0, args.cpu_nz, os.cpu_count() or 1)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {
+            "metric": metric, "value": value, "unit": "cell-updates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": dict(grid_desc, mode=args.mode, parallelism=f"replicas x{world}",
+                           l2="inputs > L2 (1 GiB FP64 fields)",
+                           picard={"radial_iters": stats["radial_iterations"],
+                                   "axial_iters": stats["axial_iterations"],
+                                   "halvings": stats["halvings"], "steps": stats["steps"]}),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": f"{dom} Picard iteration ({args.mode})",
+                         "bytes_per_launch": per_launch_bytes, "launches": dom_n,
+                         "ms_per_launch": dom_ms / max(dom_n, 1), "peak_kind": peak_kind,
+                         "other_sweep_ms_per_launch": {k: v[0] / max(v[1], 1) for k, v in
+                                                       sweeps.items()}},
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
+        }
+        print(json.dumps(line))
+    if pg:
+        pg.destroy_process_group()
+
+
+def gpu_stepper_for(case, mode, device):
+    from paper_1912_03744_b200.configs import make_source
+    from paper_1912_03744_b200.solver import AdiStepper, DevicePlan
+    g = case.grid()
+    return AdiStepper(g, case.materials, make_source(case, g), case.timing, case.solver,
+                      DevicePlan(device=device, mode=mode))
+
+
+if __name__ == "__main__":
+    main()

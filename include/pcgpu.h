@@ -1,0 +1,242 @@
+/* pcgpu.h -- C-ABI of the B200-native ADI hot path of pulsecell
+ * (arXiv 1912.03744 reference, /root/reference/proj).
+ *
+ * This is the drop-in boundary for `class pulsecell::AdiStepper`
+ * (proj/include/pulsecell/solver.hpp:66-106, proj/src/solver.cpp:125-373).
+ * Plain pointers and sizes only; no C++ exceptions cross it. Every entry point
+ * returns a pcgpu_status; the C++ wrapper (include/pulsecell_gpu/adi_stepper.hpp)
+ * and the Python mirror (paper_1912_03744_b200/solver.py) map the codes back to
+ * the reference exception types (errors.hpp:10-54).
+ *
+ * Fields are FP64, column-major nr x nz -- element (i, j) at j*nr + i -- the
+ * reference's Array2 layout (types.hpp:10-14). Field pointers passed to the
+ * half-step / step entry points are DEVICE pointers (cudaMalloc / torch);
+ * the *_host variants take host pointers and copy.
+ */
+#ifndef PCGPU_H
+#define PCGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCGPU_ABI_VERSION 1
+
+/* Status codes. Reference equivalents in brackets. */
+enum pcgpu_status {
+  PCGPU_OK = 0,
+  PCGPU_ERR_CONFIG = 1,      /* ConfigError: SolverConfig::validate (solver.cpp:33-42),
+                                stepper wiring (solver.cpp:133-138), SourceSpec (source.cpp:9-17) */
+  PCGPU_ERR_TAU_FLOOR = 2,   /* TauFloorError (solver.cpp:369-371) */
+  PCGPU_ERR_TABLE_RANGE = 3, /* TableRangeError in a line body (materials.cpp:60-69), re-thrown
+                                as LineError(lowest line) (parallel.cpp:68-93,115) */
+  PCGPU_ERR_ZERO_PIVOT = 4,  /* Error("thomas_solve: zero pivot") (tridiagonal.hpp:27,33) */
+  PCGPU_ERR_CUDA = 5,        /* CUDA runtime failure (no reference equivalent) */
+  PCGPU_ERR_ARG = 6          /* bad pointer / size at the boundary */
+};
+
+/* Enumerations mirror the reference's enum classes value-for-value. */
+enum pcgpu_halfpoint_rule { /* materials.hpp:16-20 */
+  PCGPU_HALFPOINT_MEAN_TEMPERATURE = 0,
+  PCGPU_HALFPOINT_MEAN_LAMBDA = 1,
+  PCGPU_HALFPOINT_TWO_SIDED_HARMONIC = 2
+};
+enum pcgpu_range_policy { PCGPU_RANGE_CLAMP = 0, PCGPU_RANGE_STRICT = 1 }; /* materials.hpp:14 */
+enum pcgpu_waveform { PCGPU_WAVE_RECTANGULAR = 0, PCGPU_WAVE_TRANSIENT = 1 }; /* source.hpp:9 */
+enum pcgpu_source_kind {
+  PCGPU_SOURCE_NULL = 0,   /* NullSource (source.hpp:57-61) */
+  PCGPU_SOURCE_JOULE = 1,  /* JouleSource (source.hpp:63-83) */
+  PCGPU_SOURCE_FIELD = 2   /* T-independent per-cell power (e.g. the acceptance suite's
+                              ManufacturedSource, acceptance_main.cpp:262-274): the host binds
+                              an nr x nz power array per half-step (pcgpu_bind_power_field). */
+};
+enum pcgpu_mode {
+  /* Bit-identical to the reference CPU path: the reference's operation order
+   * (SURVEY Appendix A), no FMA contraction, sequential Thomas per line. */
+  PCGPU_MODE_EXACT = 0,
+  /* Throughput mode: partitioned (chunked) line solves, FMA allowed. Agrees with
+   * the reference to roundoff (north-star tolerance 1e-9 fixed-dt / 1e-6 adaptive). */
+  PCGPU_MODE_FAST = 1
+};
+
+/* Piecewise-linear property table: n strictly increasing knots t[] and values v[]
+ * (PropertyTable, materials.hpp:24-53). n == 0 means "absent" (an empty chi). */
+typedef struct pcgpu_table {
+  int32_t n;
+  const double* t;
+  const double* v;
+} pcgpu_table;
+
+/* MaterialTable (materials.hpp:57-95): constant rho and three tables. */
+typedef struct pcgpu_material {
+  double rho;
+  pcgpu_table cv;     /* Property::HeatCapacity */
+  pcgpu_table lambda; /* Property::Conductivity */
+  pcgpu_table chi;    /* Property::Resistivity (may be empty) */
+} pcgpu_material;
+
+/* Everything the stepper needs, marshalled from the reference objects
+ * (Grid, LayerMaterials, SourceModel, SourceSpec, SolverConfig). Arrays are
+ * copied by pcgpu_create; the caller may free them afterwards. */
+typedef struct pcgpu_desc {
+  int32_t abi_version; /* must be PCGPU_ABI_VERSION */
+
+  /* Grid (geometry.hpp:48-115), metrics exactly as Grid computes them. */
+  int32_t nr, nz;          /* Grid::nr(), Grid::nz() */
+  int32_t nr_core;         /* Grid::nr_core()   -- row_extent(j) = j < nz_shared ? nr : nr_core */
+  int32_t nz_shared;       /* Grid::nz_shared() -- col_extent(i) = i < nr_core ? nz : nz_shared */
+  const int32_t* layer;    /* [nr]   Grid::layer(i) */
+  const double* r_center;  /* [nr]   Grid::r_center(i) */
+  const double* gap_r;     /* [nr+1] Grid::gap_r(i) (mirror-ghost ends) */
+  const double* width_z;   /* [nz]   Grid::width_z(j) */
+  const double* gap_z;     /* [nz+1] Grid::gap_z(j) (mirror-ghost ends) */
+
+  /* LayerMaterials: one material per layer (solver.cpp:135-138). */
+  int32_t n_layers;
+  const pcgpu_material* materials; /* [n_layers] */
+
+  /* SourceModel. amplitude = SourceSpec::current_factor() (source.hpp:26-28). */
+  int32_t source_kind;  /* pcgpu_source_kind */
+  int32_t source_layer;
+  double amplitude;
+
+  /* SourceSpec timing (source.hpp:14-29), for initial_tau / pulse_value on the host. */
+  double t_per, t_src, t_trs, xi, zeta;
+  int32_t waveform; /* pcgpu_waveform */
+
+  /* SolverConfig (solver.hpp:12-31). */
+  double epsilon;
+  int32_t max_iter;
+  double tau_min; /* <= 0 means 1e-12 * t_per (effective_tau_min) */
+  double tau_transient_divisor;
+  double tau_source_divisor;
+  int32_t halfpoint_rule; /* pcgpu_halfpoint_rule */
+  int32_t range_policy;   /* pcgpu_range_policy */
+  int32_t all_neumann;
+  double T0;
+  double t_ceiling;
+
+  /* Device options (not part of the reference schema). */
+  int32_t mode;   /* pcgpu_mode */
+  int32_t device; /* CUDA device ordinal */
+} pcgpu_desc;
+
+/* HalfStepOutcome (solver.hpp:50-54). */
+typedef struct pcgpu_outcome {
+  int32_t converged;
+  int32_t iterations;
+  double last_delta;
+} pcgpu_outcome;
+
+/* StepResult (solver.hpp:56-60). */
+typedef struct pcgpu_step_result {
+  double tau_used;
+  int32_t halvings;
+  pcgpu_outcome radial, axial;
+} pcgpu_step_result;
+
+/* Counters accumulated over a pcgpu_run: every half-step attempt's active
+ * cells x Picard iterations (SURVEY 8(d) "cell-update"), rejected attempts
+ * included; and the same for accepted attempts only. */
+typedef struct pcgpu_run_stats {
+  double t_end;
+  int64_t steps;
+  int64_t halvings;
+  int64_t radial_iterations;
+  int64_t axial_iterations;
+  double cell_updates;
+  double cell_updates_accepted;
+  double attempt_cells; /* sum over attempts of active cells (x2 half-steps) */
+} pcgpu_run_stats;
+
+typedef struct pcgpu_stepper pcgpu_stepper;
+
+/* Library / device introspection. */
+int32_t pcgpu_abi_version(void);
+int pcgpu_device_count(int32_t* count);
+
+/* AdiStepper(grid, mats, source, timing, cfg, pool) -- solver.cpp:125-160.
+ * Validates like the reference and allocates the device buffers (the
+ * reference's half_, next_, iter_buf_, expl_, kbar_). */
+int pcgpu_create(const pcgpu_desc* desc, pcgpu_stepper** out);
+void pcgpu_destroy(pcgpu_stepper* h);
+
+/* Last error message for h (or for the last failed pcgpu_create when h is NULL). */
+const char* pcgpu_last_error(const pcgpu_stepper* h);
+/* Lowest failing line of the last PCGPU_ERR_TABLE_RANGE / PCGPU_ERR_ZERO_PIVOT
+ * (LineError::line(), errors.hpp:46-54); -1 if none. */
+int64_t pcgpu_error_line(const pcgpu_stepper* h);
+
+/* Reference free function initial_tau(t, timing, cfg) (solver.cpp:44-51). */
+double pcgpu_initial_tau(const pcgpu_stepper* h, double t);
+/* Reference free function pulse_value(t, spec) (source.cpp:42-45). */
+double pcgpu_pulse_value(const pcgpu_stepper* h, double t);
+/* Active cells of the grid (Grid::active_cells, geometry.cpp:95). */
+int64_t pcgpu_active_cells(const pcgpu_stepper* h);
+
+/* Per-cell power for PCGPU_SOURCE_FIELD: device pointer, nr x nz column-major,
+ * read by the next half-step (the SourceModel::power(i, j, ...) values for the
+ * half-step's bind_time). */
+int pcgpu_bind_power_field(pcgpu_stepper* h, const double* power_dev);
+
+/* AdiStepper::radial_half_step (solver.cpp:235-257). Device pointers; out != T_cur.
+ * `out` holds the half-layer field when outcome->converged. */
+int pcgpu_radial_half_step(pcgpu_stepper* h, const double* T_cur, double t, double tau,
+                           double* out, pcgpu_outcome* outcome);
+/* AdiStepper::axial_half_step (solver.cpp:334-354). Device pointers; out != T_half. */
+int pcgpu_axial_half_step(pcgpu_stepper* h, const double* T_half, double t, double tau,
+                          double* out, pcgpu_outcome* outcome);
+/* AdiStepper::step (solver.cpp:356-373) on a device field, in place.
+ * Returns PCGPU_ERR_TAU_FLOOR when halving passes the floor. */
+int pcgpu_step(pcgpu_stepper* h, double* field, double t, pcgpu_step_result* result);
+/* Host-memory variants (H2D copy, step, D2H copy). */
+int pcgpu_step_host(pcgpu_stepper* h, double* field_host, double t, pcgpu_step_result* result);
+int pcgpu_radial_half_step_host(pcgpu_stepper* h, const double* T_cur_host, double t,
+                                double tau, double* out_host, pcgpu_outcome* outcome);
+int pcgpu_axial_half_step_host(pcgpu_stepper* h, const double* T_half_host, double t,
+                               double tau, double* out_host, pcgpu_outcome* outcome);
+
+/* nsteps calls of step() with t += tau_used (the bench harness loop,
+ * bench.cpp:20-22), keeping the field resident on the device between steps.
+ * `field` is a device pointer (in/out). Per-step results are written to
+ * `results` when non-NULL ([nsteps]). */
+int pcgpu_run(pcgpu_stepper* h, double* field, double t0, int32_t nsteps,
+              pcgpu_step_result* results, pcgpu_run_stats* stats);
+
+/* MaterialTable::clamp_events() per layer (materials.hpp:85, materials.cpp:68).
+ * counts has n_layers entries. Counted per out-of-range evaluation on the device. */
+int pcgpu_clamp_events(const pcgpu_stepper* h, uint64_t* counts);
+
+/* Stream the stepper launches on (a cudaStream_t as void*), for CUDA-event timing. */
+void* pcgpu_stream(const pcgpu_stepper* h);
+
+/* Time spent in the dominant kernel: the last run's accumulated device time
+ * (CUDA events around each launch of the Picard line kernels) and launch count. */
+int pcgpu_kernel_timing(const pcgpu_stepper* h, double* radial_ms, int64_t* radial_launches,
+                        double* axial_ms, int64_t* axial_launches);
+int pcgpu_enable_kernel_timing(pcgpu_stepper* h, int32_t on);
+/* Number of this library's kernels launched since creation. */
+int64_t pcgpu_launch_count(const pcgpu_stepper* h);
+
+/* ---- Batched tridiagonal systems (BASELINE configs[1]) ----------
+ * thomas_solve_inplace (tridiagonal.hpp:25-42) applied to `batch` independent
+ * systems of size n, all device pointers. Layouts:
+ *   PCGPU_LAYOUT_CONTIGUOUS: system s, row k at s*n + k   (line-contiguous)
+ *   PCGPU_LAYOUT_STRIDED:    system s, row k at k*batch + s (interleaved / transposed)
+ * lower[k=0] and upper[k=n-1] are ignored like the reference. x may alias rhs.
+ * `exact` = 1: the reference's operation order, bit-identical per system;
+ * 0: the fastest variant (may reorder arithmetic). Returns PCGPU_ERR_ZERO_PIVOT
+ * (error_line = lowest failing system) on a zero pivot. */
+enum pcgpu_layout { PCGPU_LAYOUT_CONTIGUOUS = 0, PCGPU_LAYOUT_STRIDED = 1 };
+int pcgpu_tridiag_batch(const double* lower, const double* diag, const double* upper,
+                        const double* rhs, double* x, int64_t n, int64_t batch,
+                        int32_t layout, int32_t exact, void* stream, int64_t* failed_system);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PCGPU_H */

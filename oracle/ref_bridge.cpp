@@ -1,0 +1,358 @@
+// ref_bridge.cpp -- TEST INFRASTRUCTURE ONLY (the checker, never the product).
+//
+// Thin C wrapper over the reference's own pulsecell library, compiled
+// unchanged from /root/reference/proj/src (see oracle/Makefile). Nothing here
+// re-implements reference arithmetic: every number comes from the reference's
+// Grid, MaterialTable, JouleSource, AdiStepper, thomas_solve_inplace and
+// LinePool. Exceptions are mapped onto pcgpu_status codes.
+#include "ref_bridge.h"
+
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "pulsecell/errors.hpp"
+#include "pulsecell/geometry.hpp"
+#include "pulsecell/materials.hpp"
+#include "pulsecell/parallel.hpp"
+#include "pulsecell/solver.hpp"
+#include "pulsecell/source.hpp"
+#include "pulsecell/tridiagonal.hpp"
+
+using namespace pulsecell;
+
+namespace {
+
+// T-independent per-cell power bound by the host (the acceptance suite's
+// ManufacturedSource pattern, acceptance_main.cpp:262-274).
+class ArraySource final : public SourceModel {
+ public:
+  ArraySource(Index nr, Index nz) : p_(static_cast<size_t>(nr * nz), 0.0), nr_(nr) {}
+  void bind_time(Real) override {}
+  Real power(Index i, Index j, int, Real) const override { return p_[j * nr_ + i]; }
+  void set(const double* p) { std::memcpy(p_.data(), p, p_.size() * sizeof(double)); }
+
+ private:
+  std::vector<double> p_;
+  Index nr_;
+};
+
+PropertyTable make_table(const pcgpu_table& t) {
+  if (t.n <= 0) return PropertyTable();
+  return PropertyTable(std::vector<Real>(t.t, t.t + t.n), std::vector<Real>(t.v, t.v + t.n));
+}
+
+int classify(const std::exception& e) {
+  if (dynamic_cast<const TauFloorError*>(&e)) return PCGPU_ERR_TAU_FLOOR;
+  if (dynamic_cast<const TableRangeError*>(&e)) return PCGPU_ERR_TABLE_RANGE;
+  if (dynamic_cast<const ConfigError*>(&e)) return PCGPU_ERR_CONFIG;
+  const std::string w = e.what();
+  if (w.find("zero pivot") != std::string::npos) return PCGPU_ERR_ZERO_PIVOT;
+  if (w.find("outside table range") != std::string::npos ||
+      w.find("property table missing") != std::string::npos)
+    return PCGPU_ERR_TABLE_RANGE;
+  return PCGPU_ERR_CONFIG;
+}
+
+thread_local std::string g_create_error;
+
+}  // namespace
+
+struct pcref {
+  DomainSpec domain;
+  GridSpec gridspec;
+  MaterialSet materials;
+  std::unique_ptr<Grid> grid;
+  LayerMaterials layers;
+  SourceSpec timing;
+  std::unique_ptr<SourceModel> source;
+  ArraySource* array_source = nullptr;
+  SolverConfig cfg;
+  std::unique_ptr<LinePool> pool;
+  std::unique_ptr<AdiStepper> stepper;
+  std::string error;
+  int64_t error_line = -1;
+
+  int fail(const std::exception& e) {
+    error = e.what();
+    error_line = -1;
+    if (auto* le = dynamic_cast<const LineError*>(&e)) error_line = le->line();
+    return classify(e);
+  }
+};
+
+extern "C" {
+
+int pcref_create(const pcref_spec* s, pcref** out) {
+  *out = nullptr;
+  auto h = std::make_unique<pcref>();
+  try {
+    for (int m = 0; m < s->n_layers; ++m) {
+      h->domain.layer_radii.push_back(s->layer_radii[m]);
+      h->domain.layer_materials.push_back("layer" + std::to_string(m));
+      h->gridspec.radial_divisions.push_back(s->radial_divisions[m]);
+    }
+    h->domain.core_length = s->core_length;
+    h->domain.outer_length = s->outer_length;
+    h->domain.source_layer = s->source_layer;
+    h->gridspec.axial_divisions_core = s->axial_divisions_core;
+    h->gridspec.axial_divisions_outer = s->axial_divisions_outer;
+    h->grid = std::make_unique<Grid>(h->domain, h->gridspec);
+    for (int m = 0; m < s->n_layers; ++m) {
+      const pcgpu_material& pm = s->materials[m];
+      h->materials.add(MaterialTable(h->domain.layer_materials[m], pm.rho, make_table(pm.cv),
+                                     make_table(pm.lambda), make_table(pm.chi)));
+    }
+    h->layers = resolve_layers(h->materials, h->domain.layer_materials);
+
+    h->timing.t_per = s->t_per;
+    h->timing.t_src = s->t_src;
+    h->timing.t_trs = s->t_trs;
+    h->timing.xi = s->xi;
+    h->timing.zeta = s->zeta;
+    h->timing.I0 = s->I0;
+    h->timing.S_C = s->S_C;
+    h->timing.waveform = s->waveform == PCGPU_WAVE_RECTANGULAR ? Waveform::Rectangular
+                                                               : Waveform::Transient;
+    h->timing.joule_dimensional = s->joule_dimensional != 0;
+    if (h->timing.S_C <= 0) h->timing.S_C = h->domain.source_cross_section();  // config.cpp:207
+
+    h->cfg.epsilon = s->epsilon;
+    h->cfg.max_iter = s->max_iter;
+    h->cfg.tau_min = s->tau_min;
+    h->cfg.tau_transient_divisor = s->tau_transient_divisor;
+    h->cfg.tau_source_divisor = s->tau_source_divisor;
+    h->cfg.halfpoint_rule = static_cast<HalfPointRule>(s->halfpoint_rule);
+    h->cfg.range_policy = static_cast<RangePolicy>(s->range_policy);
+    h->cfg.all_neumann = s->all_neumann != 0;
+    h->cfg.T0 = s->T0;
+    h->cfg.t_ceiling = s->t_ceiling;
+
+    if (s->source_kind == PCGPU_SOURCE_JOULE) {
+      h->source = std::make_unique<JouleSource>(h->timing, s->source_layer,
+                                                *h->layers[s->source_layer], h->cfg.range_policy);
+    } else if (s->source_kind == PCGPU_SOURCE_FIELD) {
+      auto a = std::make_unique<ArraySource>(h->grid->nr(), h->grid->nz());
+      h->array_source = a.get();
+      h->source = std::move(a);
+    } else {
+      h->source = std::make_unique<NullSource>();
+    }
+    ExecPlan plan;
+    plan.workers = s->workers < 1 ? 1 : s->workers;
+    plan.chunking = s->chunking == 1 ? Chunking::StaticInterleave : Chunking::StaticBlock;
+    h->pool = std::make_unique<LinePool>(plan);
+    h->stepper = std::make_unique<AdiStepper>(*h->grid, h->layers, *h->source, h->timing,
+                                              h->cfg, *h->pool);
+  } catch (const std::exception& e) {
+    g_create_error = e.what();
+    return classify(e);
+  }
+  *out = h.release();
+  return PCGPU_OK;
+}
+
+void pcref_destroy(pcref* h) { delete h; }
+
+const char* pcref_last_error(const pcref* h) {
+  return h ? h->error.c_str() : g_create_error.c_str();
+}
+
+int64_t pcref_error_line(const pcref* h) { return h->error_line; }
+
+void pcref_grid_dims(const pcref* h, int64_t* nr, int64_t* nz, int64_t* nr_core,
+                     int64_t* nz_shared, int64_t* active) {
+  const Grid& g = *h->grid;
+  *nr = g.nr();
+  *nz = g.nz();
+  *nr_core = g.nr_core();
+  *nz_shared = g.nz_shared();
+  *active = g.active_cells();
+}
+
+void pcref_grid_arrays(const pcref* h, double* r_center, double* width_r, double* gap_r,
+                       double* z_center, double* width_z, double* gap_z, int32_t* layer) {
+  const Grid& g = *h->grid;
+  for (Index i = 0; i < g.nr(); ++i) {
+    r_center[i] = g.r_center(i);
+    width_r[i] = g.width_r(i);
+    layer[i] = g.layer(i);
+  }
+  for (Index i = 0; i <= g.nr(); ++i) gap_r[i] = g.gap_r(i);
+  for (Index j = 0; j < g.nz(); ++j) {
+    z_center[j] = g.z_center(j);
+    width_z[j] = g.width_z(j);
+  }
+  for (Index j = 0; j <= g.nz(); ++j) gap_z[j] = g.gap_z(j);
+}
+
+double pcref_source_amplitude(const pcref* h) { return h->timing.current_factor(); }
+double pcref_tau_floor(const pcref* h) { return h->cfg.effective_tau_min(h->timing.t_per); }
+double pcref_initial_tau(const pcref* h, double t) { return initial_tau(t, h->timing, h->cfg); }
+double pcref_pulse_value(const pcref* h, double t) { return pulse_value(t, h->timing); }
+
+int pcref_bind_power_field(pcref* h, const double* power) {
+  if (!h->array_source) return PCGPU_ERR_ARG;
+  h->array_source->set(power);
+  return PCGPU_OK;
+}
+
+static Array2 to_array(const pcref* h, const double* p) {
+  Array2 a(h->grid->nr(), h->grid->nz());
+  std::memcpy(a.data(), p, sizeof(double) * a.size());
+  return a;
+}
+
+int pcref_radial_half_step(pcref* h, const double* T_cur, double t, double tau, double* out,
+                           pcgpu_outcome* o) {
+  try {
+    const Array2 tc = to_array(h, T_cur);
+    Array2 dst = to_array(h, out);
+    const HalfStepOutcome r = h->stepper->radial_half_step(tc, t, tau, dst);
+    std::memcpy(out, dst.data(), sizeof(double) * dst.size());
+    o->converged = r.converged;
+    o->iterations = r.iterations;
+    o->last_delta = r.last_delta;
+  } catch (const std::exception& e) {
+    return h->fail(e);
+  }
+  return PCGPU_OK;
+}
+
+int pcref_axial_half_step(pcref* h, const double* T_half, double t, double tau, double* out,
+                          pcgpu_outcome* o) {
+  try {
+    const Array2 th = to_array(h, T_half);
+    Array2 dst = to_array(h, out);
+    const HalfStepOutcome r = h->stepper->axial_half_step(th, t, tau, dst);
+    std::memcpy(out, dst.data(), sizeof(double) * dst.size());
+    o->converged = r.converged;
+    o->iterations = r.iterations;
+    o->last_delta = r.last_delta;
+  } catch (const std::exception& e) {
+    return h->fail(e);
+  }
+  return PCGPU_OK;
+}
+
+static void copy_result(const StepResult& r, pcgpu_step_result* o) {
+  o->tau_used = r.tau_used;
+  o->halvings = r.halvings;
+  o->radial.converged = r.radial.converged;
+  o->radial.iterations = r.radial.iterations;
+  o->radial.last_delta = r.radial.last_delta;
+  o->axial.converged = r.axial.converged;
+  o->axial.iterations = r.axial.iterations;
+  o->axial.last_delta = r.axial.last_delta;
+}
+
+int pcref_step(pcref* h, double* field, double t, pcgpu_step_result* result) {
+  try {
+    Array2 f = to_array(h, field);
+    const StepResult r = h->stepper->step(f, t);
+    std::memcpy(field, f.data(), sizeof(double) * f.size());
+    copy_result(r, result);
+  } catch (const std::exception& e) {
+    return h->fail(e);
+  }
+  return PCGPU_OK;
+}
+
+// nsteps x step() with t += tau_used, exactly the bench harness loop
+// (bench.cpp:20-22). Stats count the accepted attempt's iterations (step()
+// reports only those, solver.hpp:56-60).
+int pcref_run(pcref* h, double* field, double t0, int32_t nsteps, pcgpu_step_result* results,
+              pcgpu_run_stats* stats) {
+  pcgpu_run_stats st{};
+  const Grid& g = *h->grid;
+  double t = t0;
+  try {
+    Array2 f = to_array(h, field);
+    for (int32_t k = 0; k < nsteps; ++k) {
+      const StepResult r = h->stepper->step(f, t);
+      t += r.tau_used;
+      if (results) copy_result(r, &results[k]);
+      st.steps += 1;
+      st.halvings += r.halvings;
+      st.radial_iterations += r.radial.iterations;
+      st.axial_iterations += r.axial.iterations;
+      const double cells = static_cast<double>(g.active_cells());
+      st.cell_updates_accepted += cells * (r.radial.iterations + r.axial.iterations);
+      st.attempt_cells += 2.0 * cells;
+    }
+    std::memcpy(field, f.data(), sizeof(double) * f.size());
+  } catch (const std::exception& e) {
+    st.t_end = t;
+    st.cell_updates = st.cell_updates_accepted;
+    if (stats) *stats = st;
+    return h->fail(e);
+  }
+  st.t_end = t;
+  st.cell_updates = st.cell_updates_accepted;
+  if (stats) *stats = st;
+  return PCGPU_OK;
+}
+
+int pcref_clamp_events(const pcref* h, uint64_t* counts) {
+  for (size_t m = 0; m < h->layers.size(); ++m) counts[m] = h->layers[m]->clamp_events();
+  return PCGPU_OK;
+}
+
+double pcref_apply_lambda_r(const pcref* h, const double* field, int64_t i, int64_t j) {
+  return apply_lambda_r(*h->grid, h->layers, to_array(h, field), i, j, h->cfg);
+}
+double pcref_apply_lambda_z(const pcref* h, const double* field, int64_t i, int64_t j) {
+  return apply_lambda_z(*h->grid, h->layers, to_array(h, field), i, j, h->cfg);
+}
+double pcref_weighted_heat_sum(const pcref* h, const double* field) {
+  return weighted_heat_sum(*h->grid, h->layers, to_array(h, field));
+}
+
+int pcref_eval(const pcref* h, int32_t layer, int32_t prop, double T, double* value) {
+  try {
+    *value = h->layers[layer]->eval(static_cast<Property>(prop), T, h->cfg.range_policy);
+  } catch (const std::exception& e) {
+    return classify(e);
+  }
+  return PCGPU_OK;
+}
+
+int pcref_thomas_batch(const double* lower, const double* diag, const double* upper,
+                       const double* rhs, double* x, int64_t n, int64_t batch, int32_t layout,
+                       int32_t workers, int64_t* failed_system) {
+  *failed_system = -1;
+  try {
+    ExecPlan plan;
+    plan.workers = workers < 1 ? 1 : workers;
+    LinePool pool(plan);
+    pool.for_lines(batch, [&](Index s) {
+      thread_local std::vector<double> a, b, c, d, xx, w;
+      if (layout == PCGPU_LAYOUT_CONTIGUOUS) {
+        w.resize(static_cast<size_t>(n));
+        const size_t off = static_cast<size_t>(s) * static_cast<size_t>(n);
+        thomas_solve_inplace(lower + off, diag + off, upper + off, rhs + off, x + off,
+                             w.data(), n);
+      } else {
+        // Strided layout: gather the line, solve, scatter (the reference's
+        // axial_line pattern, solver.cpp:293-299,325-330).
+        a.resize(n); b.resize(n); c.resize(n); d.resize(n); xx.resize(n); w.resize(n);
+        for (Index k = 0; k < n; ++k) {
+          const size_t idx = static_cast<size_t>(k) * static_cast<size_t>(batch) + s;
+          a[k] = lower[idx]; b[k] = diag[idx]; c[k] = upper[idx]; d[k] = rhs[idx];
+        }
+        thomas_solve_inplace(a.data(), b.data(), c.data(), d.data(), xx.data(), w.data(), n);
+        for (Index k = 0; k < n; ++k)
+          x[static_cast<size_t>(k) * static_cast<size_t>(batch) + s] = xx[k];
+      }
+    });
+  } catch (const LineError& e) {
+    *failed_system = e.line();
+    return PCGPU_ERR_ZERO_PIVOT;
+  } catch (const std::exception& e) {
+    return classify(e);
+  }
+  return PCGPU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,58 @@
+// adi_kernels.h -- host-side launcher declarations for the ADI kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "adi_device.cuh"
+
+namespace pcgpu {
+
+// Field layouts (both nr x nz FP64):
+//   N ("natural", the reference's Array2): (i, j) at j*nr + i -- r-lines contiguous.
+//   T ("transposed"):                      (i, j) at i*nz + j -- z-lines contiguous.
+
+// ---- exact mode (bit-identical to the reference; adi_exact.cu, --fmad=false) ----
+
+// K3 explicit_axial_pass (solver.cpp:162-189): explT = Lambda_z[srcN]; also
+// writes srcT = transpose(srcN) (the anchor for the T-layout radial sweep).
+void launch_explicit_axial_exact(const DevProblem& P, const double* srcN, double* explT,
+                                 double* srcT, DevStatus* st, cudaStream_t s);
+// K1 one Picard iteration of the radial sweep (solver.cpp:191-233, :245-248),
+// T layout, thread per radial line. Early-exits when iteration it-1 converged.
+void launch_radial_exact(const DevProblem& P, int it, double eps, double half_k, double pulse,
+                         const double* TsT, const double* TcT, const double* explT,
+                         const double* powT, double* outT, double* wT, double* xT,
+                         DevStatus* st, cudaStream_t s);
+// K4 axial_fixed_rhs_pass (solver.cpp:259-284) from the T-layout half field:
+// kbarN, explN and halfN (transposed copy) in N layout.
+void launch_axial_rhs_exact(const DevProblem& P, double half_k, double pulse,
+                            const double* halfT, const double* powN, double* kbarN,
+                            double* explN, double* halfN, DevStatus* st, cudaStream_t s);
+// K2 one Picard iteration of the axial sweep (solver.cpp:286-332, :343-345),
+// N layout, thread per axial line.
+void launch_axial_exact(const DevProblem& P, int it, double eps, const double* TsN,
+                        const double* ThN, const double* kbarN, const double* explN,
+                        double* outN, double* wN, double* xN, DevStatus* st, cudaStream_t s);
+
+// ---- layout helpers (masked: only in-mask cells are written) ----
+void launch_transpose_N2T(const DevProblem& P, const double* srcN, double* dstT, cudaStream_t s);
+void launch_transpose_T2N(const DevProblem& P, const double* srcT, double* dstN, cudaStream_t s);
+
+// ---- fast mode (adi_fast.cu) ----
+bool fast_supported(const DevProblem& P);
+void launch_radial_fast(const DevProblem& P, int it, double eps, double half_k, double pulse,
+                        const double* TsN, const double* TcN, const double* explN,
+                        const double* powN, double* outN, DevStatus* st, cudaStream_t s);
+void launch_explicit_axial_fast(const DevProblem& P, const double* srcN, double* explN,
+                                DevStatus* st, cudaStream_t s);
+void launch_axial_rhs_fast(const DevProblem& P, double half_k, double pulse, const double* halfN,
+                           const double* powN, double* kbarT, double* explT, double* halfT,
+                           DevStatus* st, cudaStream_t s);
+void launch_axial_fast(const DevProblem& P, int it, double eps, const double* TsT,
+                       const double* ThT, const double* kbarT, const double* explT,
+                       double* outT, DevStatus* st, cudaStream_t s);
+
+// Kernel launch counter (for the bench's gpu_launches claim).
+extern unsigned long long g_launches;
+
+}  // namespace pcgpu

@@ -1,0 +1,779 @@
+// pcgpu.cu -- host side of the C-ABI (include/pcgpu.h): the B200 AdiStepper.
+//
+// Mirrors pulsecell::AdiStepper (solver.hpp:66-106, solver.cpp:125-373):
+//   ctor          -> pcgpu_create   (validation solver.cpp:33-42,133-138; buffers :140-159)
+//   radial/axial  -> pcgpu_*_half_step (Picard loops solver.cpp:235-257, :334-354)
+//   step          -> pcgpu_step     (tau halving controller solver.cpp:356-373)
+// The Picard iterations run on the device; each iteration kernel early-exits
+// once the previous iteration's device-side max-norm passed (< epsilon), so
+// the host enqueues a predicted batch of iterations and synchronises once per
+// half-step to read the outcome (no per-iteration round trip).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/pcgpu.h"
+#include "adi_kernels.h"
+
+using namespace pcgpu;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct CudaError {
+  cudaError_t e;
+  const char* what;
+};
+
+#define CK(x)                                           \
+  do {                                                  \
+    cudaError_t e_ = (x);                               \
+    if (e_ != cudaSuccess) throw CudaError{e_, #x};     \
+  } while (0)
+
+// Host restatement of pulse_value (source.cpp:18-45) -- same libm calls as
+// the reference, so the same bits.
+double host_pulse_value(const pcgpu_desc& d, double t) {
+  const double phase = std::fmod(t, d.t_per);
+  if (d.waveform == PCGPU_WAVE_RECTANGULAR) return phase < d.t_src ? 1.0 : 0.0;
+  const double margin = d.t_trs / d.zeta * (1.0 + 6.5 / d.xi);
+  const long elapsed = std::llround((t - phase) / d.t_per);
+  const long back_hi =
+      std::min(elapsed, 1 + static_cast<long>(std::ceil((d.t_src + margin) / d.t_per)));
+  const double scale = d.xi * d.zeta / d.t_trs;
+  double sum = 0.0;
+  for (long m = -1; m <= back_hi; ++m) {
+    const double u = phase + static_cast<double>(m) * d.t_per;
+    sum += std::erf(scale * u - d.xi) - std::erf(scale * (u - d.t_src) - d.xi);
+  }
+  return 0.5 * sum;
+}
+
+// initial_tau (solver.cpp:44-51).
+double host_initial_tau(const pcgpu_desc& d, double t) {
+  const double phase = std::fmod(t, d.t_per);
+  const bool in_transient =
+      phase <= d.t_trs || (phase >= d.t_src && phase <= d.t_src + d.t_trs);
+  return in_transient ? d.t_trs / d.tau_transient_divisor : d.t_src / d.tau_source_divisor;
+}
+
+std::string validate(const pcgpu_desc* d) {
+  if (d->abi_version != PCGPU_ABI_VERSION) return "pcgpu: ABI version mismatch";
+  // SolverConfig::validate (solver.cpp:33-42)
+  if (!(d->epsilon > 0)) return "solver.epsilon: must be > 0";
+  if (d->max_iter < 1) return "solver.max_iter: must be >= 1";
+  if (d->max_iter > kMaxIter) return "solver.max_iter: exceeds the device limit";
+  if (!(d->tau_transient_divisor > 0)) return "solver.tau_transient_divisor: must be > 0";
+  if (!(d->tau_source_divisor > 0)) return "solver.tau_source_divisor: must be > 0";
+  if (!(d->T0 > 0)) return "solver.T0: must be > 0";
+  if (!(d->t_ceiling > d->T0)) return "solver.t_ceiling: must exceed T0";
+  // SourceSpec::validate (source.cpp:9-17)
+  if (!(d->t_per > 0)) return "source.t_per: must be > 0";
+  if (!(d->t_src > 0 && d->t_src <= d->t_per))
+    return "source.t_src: must satisfy 0 < t_src <= t_per";
+  if (!(d->t_trs > 0 && d->t_trs < d->t_src)) return "source.t_trs: must satisfy 0 < t_trs < t_src";
+  if (!(d->xi > 0)) return "source.xi: must be > 0";
+  if (!(d->zeta > 0)) return "source.zeta: must be > 0";
+  // Grid / wiring (solver.cpp:135-138)
+  if (d->nr < 1 || d->nz < 1 || d->nr_core < 1 || d->nr_core > d->nr || d->nz_shared < 1 ||
+      d->nz_shared > d->nz)
+    return "stepper: invalid grid extents";
+  if (!d->layer || !d->r_center || !d->gap_r || !d->width_z || !d->gap_z)
+    return "stepper: null grid array";
+  if (d->n_layers < 1 || d->n_layers > kMaxLayers) return "stepper: one material required per layer";
+  if (!d->materials) return "stepper: null material";
+  for (int i = 0; i < d->nr; ++i)
+    if (d->layer[i] < 0 || d->layer[i] >= d->n_layers)
+      return "stepper: one material required per layer";
+  // MaterialTable / PropertyTable invariants (materials.cpp:5-37)
+  for (int m = 0; m < d->n_layers; ++m) {
+    const pcgpu_material& mt = d->materials[m];
+    if (!(mt.rho > 0)) return "material: rho must be > 0";
+    if (mt.cv.n < 1) return "material: missing heat capacity table";
+    if (mt.lambda.n < 1) return "material: missing conductivity table";
+    const pcgpu_table* tabs[3] = {&mt.cv, &mt.lambda, &mt.chi};
+    for (int p = 0; p < 3; ++p) {
+      const pcgpu_table& t = *tabs[p];
+      if (t.n < 0 || (t.n > 0 && (!t.t || !t.v))) return "property table: bad pointer";
+      for (int k = 1; k < t.n; ++k)
+        if (!(t.t[k] > t.t[k - 1]))
+          return "property table: temperature knots must be strictly increasing";
+      for (int k = 0; k < t.n; ++k) {
+        if (p < 2 && !(t.v[k] > 0)) return "material: values must be > 0";
+        if (p == 2 && t.v[k] < 0) return "material: resistivity values must be >= 0";
+      }
+    }
+  }
+  if (d->source_kind == PCGPU_SOURCE_JOULE) {
+    if (d->source_layer < 0 || d->source_layer >= d->n_layers)
+      return "domain.source_layer: out of range";
+    if (!std::isfinite(d->amplitude)) return "source.S_C: must be > 0";
+    if (d->amplitude != 0.0 && d->materials[d->source_layer].chi.n == 0)
+      return "material: source layer needs a resistivity table";
+  } else if (d->source_kind != PCGPU_SOURCE_NULL && d->source_kind != PCGPU_SOURCE_FIELD) {
+    return "source: unknown kind";
+  }
+  if (d->mode != PCGPU_MODE_EXACT && d->mode != PCGPU_MODE_FAST) return "pcgpu: unknown mode";
+  return "";
+}
+
+template <typename T>
+T* dev_upload(const std::vector<T>& v) {
+  T* p = nullptr;
+  CK(cudaMalloc(&p, sizeof(T) * std::max<size_t>(1, v.size())));
+  if (!v.empty()) CK(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  return p;
+}
+
+}  // namespace
+
+// Buffer roles. N = natural layout, T = transposed.
+enum Buf {
+  kTcT = 0,     // radial: transposed anchor T_cur   | axial: halfN
+  kExpl,        // radial: Lambda_z[T_cur] (T)       | axial: expl (N)
+  kHalfT,       // radial iterate / result (T)
+  kIterT,       // radial ping-pong (T)              | axial: ping-pong (N)
+  kW,           // Thomas work vector (exact mode)
+  kX,           // Thomas x vector (exact mode)
+  kKbar,        // axial: kbar (N)
+  kNext,        // axial result (N)
+  kField,       // pcgpu_run: resident field (N)
+  kPowN,        // bound power field (N)
+  kPowT,        // bound power field (T)
+  kNumBufs
+};
+
+struct pcgpu_stepper {
+  pcgpu_desc d{};
+  DevProblem P{};
+  std::vector<void*> dev_allocs;
+  cudaStream_t stream = nullptr;
+  DevStatus* st = nullptr;       // device
+  DevStatus* st_host = nullptr;  // pinned mirror
+  double* buf[kNumBufs] = {};
+  double tau_floor = 0;
+  int64_t active = 0;
+  std::string err;
+  int64_t err_line = -1;
+  int pred_radial = 1, pred_axial = 1;
+  bool power_bound = false;
+  // kernel timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  struct Timed { cudaEvent_t a, b; int sweep; int it; };
+  std::vector<Timed> pending;
+  double radial_ms = 0, axial_ms = 0;
+  int64_t radial_launches = 0, axial_launches = 0;
+  unsigned long long launches0 = 0;
+
+  ~pcgpu_stepper() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (auto& e : ev_pool) cudaEventDestroy(e);
+    for (void* p : dev_allocs) cudaFree(p);
+    if (st_host) cudaFreeHost(st_host);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  int fail(int code, const std::string& msg, int64_t line = -1) {
+    err = msg;
+    err_line = line;
+    return code;
+  }
+
+  size_t cells() const { return static_cast<size_t>(d.nr) * static_cast<size_t>(d.nz); }
+
+  cudaEvent_t event() {
+    if (ev_used == ev_pool.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+  }
+
+  void reset_status() {
+    // delta slots -> 0 (+0.0), err -> kNoError
+    CK(cudaMemsetAsync(st->delta, 0, sizeof(st->delta), stream));
+    CK(cudaMemsetAsync(&st->err, 0xff, sizeof(st->err), stream));
+  }
+
+  // Fetch delta[1..n] and err from the device (one sync).
+  void fetch_status(int n) {
+    CK(cudaMemcpyAsync(st_host->delta, st->delta, sizeof(unsigned long long) * (n + 1),
+                       cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(&st_host->err, &st->err, sizeof(st->err), cudaMemcpyDeviceToHost,
+                       stream));
+    CK(cudaStreamSynchronize(stream));
+  }
+
+  double delta_of(int it) const {
+    double v;
+    std::memcpy(&v, &st_host->delta[it], sizeof v);
+    return v;
+  }
+
+  int check_line_error() {
+    const unsigned long long e = st_host->err;
+    if (e == kNoError) return PCGPU_OK;
+    const int code = static_cast<int>(e & 7ull);
+    const int64_t line = static_cast<int64_t>(e >> 3);
+    const char* what = code == PCGPU_ERR_ZERO_PIVOT ? "thomas_solve: zero pivot"
+                                                    : "property table range violation";
+    return fail(code, "line " + std::to_string(line) + " failed: " + what, line);
+  }
+
+  double pulse_for(double t, double tau) const {
+    // SourceModel::bind_time(t + tau/2) (solver.cpp:238, :337)
+    return d.source_kind == PCGPU_SOURCE_JOULE ? host_pulse_value(d, t + 0.5 * tau) : 0.0;
+  }
+
+  void timed_begin(int sweep, int it, cudaEvent_t* a) {
+    if (!timing) return;
+    *a = event();
+    CK(cudaEventRecord(*a, stream));
+    (void)sweep;
+    (void)it;
+  }
+  void timed_end(int sweep, int it, cudaEvent_t a) {
+    if (!timing) return;
+    cudaEvent_t b = event();
+    CK(cudaEventRecord(b, stream));
+    pending.push_back({a, b, sweep, it});
+  }
+  // After a sync: accumulate the durations of the iterations that ran.
+  void collect_timing(int sweep, int ran) {
+    if (!timing) return;
+    std::vector<Timed> keep;
+    for (const Timed& t : pending) {
+      if (t.sweep != sweep) { keep.push_back(t); continue; }
+      if (t.it <= ran) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, t.a, t.b));
+        if (sweep == 0) { radial_ms += ms; ++radial_launches; }
+        else { axial_ms += ms; ++axial_launches; }
+      }
+    }
+    pending.swap(keep);
+    if (pending.empty()) ev_used = 0;
+  }
+
+  // ---- Picard loop driver shared by both sweeps ----------------------------
+  // `launch(it)` enqueues iteration it; returns the converged iteration or 0.
+  template <typename Launch>
+  int picard(int sweep, int& pred, Launch&& launch, pcgpu_outcome* o) {
+    const int max_iter = d.max_iter;
+    int launched = 0;
+    int batch = std::min(max_iter, std::max(1, pred) + 1);
+    o->converged = 0;
+    o->iterations = 0;
+    o->last_delta = 0;
+    while (launched < max_iter) {
+      const int upto = std::min(max_iter, launched + batch);
+      for (int it = launched + 1; it <= upto; ++it) {
+        cudaEvent_t a = nullptr;
+        timed_begin(sweep, it, &a);
+        launch(it);
+        timed_end(sweep, it, a);
+      }
+      launched = upto;
+      fetch_status(launched);
+      int rc = check_line_error();
+      if (rc) {
+        collect_timing(sweep, launched);
+        return -rc;
+      }
+      for (int it = 1; it <= launched; ++it) {
+        const double dl = delta_of(it);
+        if (dl < d.epsilon) {
+          o->converged = 1;
+          o->iterations = it;
+          o->last_delta = dl;
+          pred = it;
+          collect_timing(sweep, it);
+          return it;
+        }
+      }
+      batch = 2;
+    }
+    o->iterations = max_iter;
+    o->last_delta = delta_of(max_iter);
+    collect_timing(sweep, max_iter);
+    return 0;
+  }
+
+  // Radial half-step from an N-layout anchor. On success *resT points at the
+  // T-layout result buffer (exact mode) / N-layout (fast mode).
+  int radial(const double* TcN, double t, double tau, const double** res, pcgpu_outcome* o) {
+    const double pulse = pulse_for(t, tau);
+    const double hk = 2.0 / tau;
+    reset_status();
+    if (d.mode == PCGPU_MODE_EXACT) {
+      launch_explicit_axial_exact(P, TcN, buf[kExpl], buf[kTcT], st, stream);
+      auto src_of = [&](int it) -> const double* {
+        return it == 1 ? buf[kTcT] : (it % 2 == 0 ? buf[kHalfT] : buf[kIterT]);
+      };
+      auto dst_of = [&](int it) -> double* { return it % 2 == 1 ? buf[kHalfT] : buf[kIterT]; };
+      const int conv = picard(0, pred_radial, [&](int it) {
+        launch_radial_exact(P, it, d.epsilon, hk, pulse, src_of(it), buf[kTcT], buf[kExpl],
+                            buf[kPowT], dst_of(it), buf[kW], buf[kX], st, stream);
+      }, o);
+      if (conv < 0) return -conv;
+      if (conv > 0) *res = dst_of(conv);
+      return PCGPU_OK;
+    }
+    // fast mode: N layout throughout the radial sweep.
+    launch_explicit_axial_fast(P, TcN, buf[kExpl], st, stream);
+    auto src_of = [&](int it) -> const double* {
+      return it == 1 ? TcN : (it % 2 == 0 ? buf[kHalfT] : buf[kIterT]);
+    };
+    auto dst_of = [&](int it) -> double* { return it % 2 == 1 ? buf[kHalfT] : buf[kIterT]; };
+    const int conv = picard(0, pred_radial, [&](int it) {
+      launch_radial_fast(P, it, d.epsilon, hk, pulse, src_of(it), TcN, buf[kExpl], buf[kPowN],
+                         dst_of(it), st, stream);
+    }, o);
+    if (conv < 0) return -conv;
+    if (conv > 0) *res = dst_of(conv);
+    return PCGPU_OK;
+  }
+
+  // Axial half-step from the radial result (layout per mode). `out` (N) is
+  // the preferred destination; *res receives the N-layout buffer holding the
+  // result (out or the ping-pong buffer).
+  int axial(const double* half, double t, double tau, double* out, const double** res,
+            pcgpu_outcome* o) {
+    const double pulse = pulse_for(t, tau);
+    const double hk = 2.0 / tau;
+    reset_status();
+    if (d.mode == PCGPU_MODE_EXACT) {
+      double* halfN = buf[kTcT];
+      launch_axial_rhs_exact(P, hk, pulse, half, buf[kPowN], buf[kKbar], buf[kExpl], halfN, st,
+                             stream);
+      auto src_of = [&](int it) -> const double* {
+        return it == 1 ? halfN : (it % 2 == 0 ? out : buf[kIterT]);
+      };
+      auto dst_of = [&](int it) -> double* { return it % 2 == 1 ? out : buf[kIterT]; };
+      const int conv = picard(1, pred_axial, [&](int it) {
+        launch_axial_exact(P, it, d.epsilon, src_of(it), halfN, buf[kKbar], buf[kExpl],
+                           dst_of(it), buf[kW], buf[kX], st, stream);
+      }, o);
+      if (conv < 0) return -conv;
+      if (conv > 0) *res = dst_of(conv);
+      return PCGPU_OK;
+    }
+    // fast mode: the z-sweep runs on the T layout; results transposed back.
+    double* halfT = buf[kTcT];
+    launch_axial_rhs_fast(P, hk, pulse, half, buf[kPowN], buf[kKbar], buf[kExpl], halfT, st,
+                          stream);
+    auto src_of = [&](int it) -> const double* {
+      return it == 1 ? halfT : (it % 2 == 0 ? buf[kX] : buf[kIterT]);
+    };
+    auto dst_of = [&](int it) -> double* { return it % 2 == 1 ? buf[kX] : buf[kIterT]; };
+    const int conv = picard(1, pred_axial, [&](int it) {
+      launch_axial_fast(P, it, d.epsilon, src_of(it), halfT, buf[kKbar], buf[kExpl],
+                        dst_of(it), st, stream);
+    }, o);
+    if (conv < 0) return -conv;
+    if (conv > 0) {
+      launch_transpose_T2N(P, dst_of(conv), out, stream);
+      *res = out;
+    }
+    return PCGPU_OK;
+  }
+
+  // step(): tau controller (solver.cpp:356-373). `field` is N layout; on
+  // acceptance *accepted holds the N-layout buffer with the new field.
+  int step(const double* field, double t, double* next, const double** accepted,
+           pcgpu_step_result* r, double* attempt_updates) {
+    double tau = host_initial_tau(d, t);
+    std::memset(r, 0, sizeof *r);
+    for (;;) {
+      const double* half = nullptr;
+      int rc = radial(field, t, tau, &half, &r->radial);
+      if (rc) return rc;
+      *attempt_updates += static_cast<double>(active) * r->radial.iterations;
+      if (r->radial.converged) {
+        rc = axial(half, t, tau, next, accepted, &r->axial);
+        if (rc) return rc;
+        *attempt_updates += static_cast<double>(active) * r->axial.iterations;
+        if (r->axial.converged) {
+          r->tau_used = tau;
+          return PCGPU_OK;
+        }
+      }
+      tau *= 0.5;
+      ++r->halvings;
+      if (tau < tau_floor) {
+        char msg[160];
+        std::snprintf(msg, sizeof msg, "time step %f fell below floor %f at t=%f", tau,
+                      tau_floor, t);
+        return fail(PCGPU_ERR_TAU_FLOOR, msg);
+      }
+      r->axial = pcgpu_outcome{};
+    }
+  }
+};
+
+#define GUARD_BEGIN try {
+#define GUARD_END(h)                                                                  \
+  }                                                                                   \
+  catch (const CudaError& ce) {                                                       \
+    return (h)->fail(PCGPU_ERR_CUDA, std::string(ce.what) + ": " + cudaGetErrorString(ce.e)); \
+  }
+
+extern "C" {
+
+int32_t pcgpu_abi_version(void) { return PCGPU_ABI_VERSION; }
+
+int pcgpu_device_count(int32_t* count) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+  *count = n;
+  return PCGPU_OK;
+}
+
+int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
+  if (!d || !out) return PCGPU_ERR_ARG;
+  *out = nullptr;
+  const std::string v = validate(d);
+  if (!v.empty()) {
+    g_create_error = v;
+    return PCGPU_ERR_CONFIG;
+  }
+  auto h = std::make_unique<pcgpu_stepper>();
+  try {
+    h->d = *d;
+    CK(cudaSetDevice(d->device));
+    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    const int nr = d->nr, nz = d->nz;
+    h->tau_floor = d->tau_min > 0 ? d->tau_min : 1e-12 * d->t_per;  // solver.hpp:28-30
+    for (int i = 0; i < nr; ++i) h->active += (i < d->nr_core ? nz : d->nz_shared);
+
+    // Metric reciprocals exactly as the reference stepper computes them
+    // (solver.cpp:146-159; geometry.hpp:87-94). Host code is compiled with
+    // -ffp-contract=off, so these are the reference's bits.
+    std::vector<double> face_r_lo(nr), inv_gap_r(nr + 1), inv_vol_r(nr);
+    std::vector<double> inv_gap_z(nz + 1), inv_eta(nz), control_z(nz), gap_z(nz + 1), width_z(nz);
+    for (int i = 0; i < nr; ++i) {
+      face_r_lo[i] = i == 0 ? 0.0 : 0.5 * (d->r_center[i - 1] + d->r_center[i]);
+      const double control_r = 0.5 * (d->gap_r[i] + d->gap_r[i + 1]);
+      inv_vol_r[i] = 1.0 / (d->r_center[i] * control_r);
+      inv_gap_r[i] = 1.0 / d->gap_r[i];
+    }
+    inv_gap_r[nr] = 1.0 / d->gap_r[nr];
+    for (int j = 0; j < nz; ++j) {
+      control_z[j] = 0.5 * (d->gap_z[j] + d->gap_z[j + 1]);
+      inv_eta[j] = 1.0 / control_z[j];
+      inv_gap_z[j] = 1.0 / d->gap_z[j];
+      width_z[j] = d->width_z[j];
+    }
+    inv_gap_z[nz] = 1.0 / d->gap_z[nz];
+    for (int j = 0; j <= nz; ++j) gap_z[j] = d->gap_z[j];
+    std::vector<int> layer(d->layer, d->layer + nr);
+
+    // Tables, flattened.
+    std::vector<double> knots, vals;
+    DevProblem& P = h->P;
+    P.n_layers = d->n_layers;
+    for (int m = 0; m < d->n_layers; ++m) {
+      const pcgpu_material& mt = d->materials[m];
+      P.mats[m].rho = mt.rho;
+      const pcgpu_table* tabs[3] = {&mt.cv, &mt.lambda, &mt.chi};
+      for (int p = 0; p < 3; ++p) {
+        const pcgpu_table& t = *tabs[p];
+        P.mats[m].off[p] = static_cast<int>(knots.size());
+        P.mats[m].n[p] = t.n;
+        P.mats[m].uniform[p] = 0;
+        P.mats[m].inv_h[p] = 0.0;
+        for (int k = 0; k < t.n; ++k) {
+          knots.push_back(t.t[k]);
+          vals.push_back(t.v[k]);
+        }
+        if (t.n >= 3) {
+          // Uniform-knot bracket guess (exactness is kept by the device fix-up).
+          const double inv_h = (t.n - 1) / (t.t[t.n - 1] - t.t[0]);
+          double worst = 0;
+          for (int k = 0; k < t.n; ++k)
+            worst = std::max(worst, std::fabs((t.t[k] - t.t[0]) * inv_h - k));
+          if (worst < 0.25) {
+            P.mats[m].uniform[p] = 1;
+            P.mats[m].inv_h[p] = inv_h;
+          }
+        }
+      }
+    }
+    P.nr = nr;
+    P.nz = nz;
+    P.nr_core = d->nr_core;
+    P.nz_shared = d->nz_shared;
+    auto up = [&](const std::vector<double>& v) {
+      double* p = dev_upload(v);
+      h->dev_allocs.push_back(p);
+      return p;
+    };
+    int* dlayer = dev_upload(layer);
+    h->dev_allocs.push_back(dlayer);
+    P.layer = dlayer;
+    P.face_r_lo = up(face_r_lo);
+    P.inv_gap_r = up(inv_gap_r);
+    P.inv_vol_r = up(inv_vol_r);
+    P.gap_z = up(gap_z);
+    P.inv_gap_z = up(inv_gap_z);
+    P.inv_eta = up(inv_eta);
+    P.control_z = up(control_z);
+    P.width_z = up(width_z);
+    P.knots = up(knots);
+    P.vals = up(vals);
+    P.source_kind = d->source_kind;
+    P.source_layer = d->source_layer;
+    P.amplitude = d->amplitude;
+    P.halfpoint_rule = d->halfpoint_rule;
+    P.range_policy = d->range_policy;
+    P.all_neumann = d->all_neumann;
+    P.T0 = d->T0;
+    unsigned long long* clamp = nullptr;
+    CK(cudaMalloc(&clamp, sizeof(unsigned long long) * d->n_layers));
+    CK(cudaMemset(clamp, 0, sizeof(unsigned long long) * d->n_layers));
+    h->dev_allocs.push_back(clamp);
+    P.clamp = clamp;
+
+    CK(cudaMalloc(&h->st, sizeof(DevStatus)));
+    h->dev_allocs.push_back(h->st);
+    CK(cudaMallocHost(&h->st_host, sizeof(DevStatus)));
+
+    // Field buffers (the reference's half_, next_, iter_buf_, expl_, kbar_,
+    // solver.cpp:140-144, plus the layout copies and Thomas work vectors).
+    // Filled with T0 like the reference's half_/next_/iter_buf_.
+    const size_t bytes = sizeof(double) * h->cells();
+    std::vector<double> t0fill(h->cells(), d->T0);
+    for (int b = 0; b < kNumBufs; ++b) {
+      if ((b == kPowN || b == kPowT) && d->source_kind != PCGPU_SOURCE_FIELD) continue;
+      double* p = nullptr;
+      CK(cudaMalloc(&p, bytes));
+      h->dev_allocs.push_back(p);
+      CK(cudaMemcpy(p, t0fill.data(), bytes, cudaMemcpyHostToDevice));
+      h->buf[b] = p;
+    }
+    CK(cudaDeviceSynchronize());
+    h->launches0 = g_launches;
+  } catch (const CudaError& ce) {
+    g_create_error = std::string(ce.what) + ": " + cudaGetErrorString(ce.e);
+    return PCGPU_ERR_CUDA;
+  }
+  *out = h.release();
+  return PCGPU_OK;
+}
+
+void pcgpu_destroy(pcgpu_stepper* h) { delete h; }
+
+const char* pcgpu_last_error(const pcgpu_stepper* h) {
+  return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+int64_t pcgpu_error_line(const pcgpu_stepper* h) { return h ? h->err_line : -1; }
+
+double pcgpu_initial_tau(const pcgpu_stepper* h, double t) { return host_initial_tau(h->d, t); }
+double pcgpu_pulse_value(const pcgpu_stepper* h, double t) { return host_pulse_value(h->d, t); }
+int64_t pcgpu_active_cells(const pcgpu_stepper* h) { return h->active; }
+void* pcgpu_stream(const pcgpu_stepper* h) { return h->stream; }
+int64_t pcgpu_launch_count(const pcgpu_stepper* h) {
+  return static_cast<int64_t>(g_launches - h->launches0);
+}
+
+int pcgpu_bind_power_field(pcgpu_stepper* h, const double* power_dev) {
+  if (h->d.source_kind != PCGPU_SOURCE_FIELD || !power_dev)
+    return h->fail(PCGPU_ERR_ARG, "bind_power_field: source kind is not FIELD");
+  GUARD_BEGIN
+  CK(cudaMemcpyAsync(h->buf[kPowN], power_dev, sizeof(double) * h->cells(),
+                     cudaMemcpyDeviceToDevice, h->stream));
+  launch_transpose_N2T(h->P, h->buf[kPowN], h->buf[kPowT], h->stream);
+  h->power_bound = true;
+  GUARD_END(h)
+  return PCGPU_OK;
+}
+
+int pcgpu_radial_half_step(pcgpu_stepper* h, const double* T_cur, double t, double tau,
+                           double* out, pcgpu_outcome* o) {
+  if (!h || !T_cur || !out || !o || out == T_cur) return PCGPU_ERR_ARG;
+  GUARD_BEGIN
+  const double* res = nullptr;
+  const int rc = h->radial(T_cur, t, tau, &res, o);
+  if (rc) return rc;
+  if (o->converged) {
+    if (h->d.mode == PCGPU_MODE_EXACT)
+      launch_transpose_T2N(h->P, res, out, h->stream);
+    else
+      CK(cudaMemcpyAsync(out, res, sizeof(double) * h->cells(), cudaMemcpyDeviceToDevice,
+                         h->stream));
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  GUARD_END(h)
+  return PCGPU_OK;
+}
+
+int pcgpu_axial_half_step(pcgpu_stepper* h, const double* T_half, double t, double tau,
+                          double* out, pcgpu_outcome* o) {
+  if (!h || !T_half || !out || !o || out == T_half) return PCGPU_ERR_ARG;
+  GUARD_BEGIN
+  const double* half = T_half;
+  if (h->d.mode == PCGPU_MODE_EXACT) {
+    launch_transpose_N2T(h->P, T_half, h->buf[kHalfT], h->stream);
+    half = h->buf[kHalfT];
+  }
+  const double* res = nullptr;
+  const int rc = h->axial(half, t, tau, out, &res, o);
+  if (rc) return rc;
+  if (o->converged && res != out)
+    CK(cudaMemcpyAsync(out, res, sizeof(double) * h->cells(), cudaMemcpyDeviceToDevice,
+                       h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  GUARD_END(h)
+  return PCGPU_OK;
+}
+
+int pcgpu_step(pcgpu_stepper* h, double* field, double t, pcgpu_step_result* r) {
+  if (!h || !field || !r) return PCGPU_ERR_ARG;
+  GUARD_BEGIN
+  const double* acc = nullptr;
+  double upd = 0;
+  const int rc = h->step(field, t, h->buf[kNext], &acc, r, &upd);
+  if (rc) return rc;
+  // field.swap(next_) (solver.cpp:364): the caller's array receives the result.
+  CK(cudaMemcpyAsync(field, acc, sizeof(double) * h->cells(), cudaMemcpyDeviceToDevice,
+                     h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  GUARD_END(h)
+  return PCGPU_OK;
+}
+
+int pcgpu_run(pcgpu_stepper* h, double* field, double t0, int32_t nsteps,
+              pcgpu_step_result* results, pcgpu_run_stats* stats) {
+  if (!h || !field || nsteps < 0) return PCGPU_ERR_ARG;
+  pcgpu_run_stats s{};
+  double t = t0;
+  int rc = PCGPU_OK;
+  GUARD_BEGIN
+  // Resident field: rotate buffer roles instead of copying per step.
+  double* cur = h->buf[kField];
+  double* nxt = h->buf[kNext];
+  double* spare = h->buf[kIterT];
+  CK(cudaMemcpyAsync(cur, field, sizeof(double) * h->cells(), cudaMemcpyDeviceToDevice,
+                     h->stream));
+  for (int32_t k = 0; k < nsteps; ++k) {
+    pcgpu_step_result r;
+    const double* acc = nullptr;
+    double upd = 0;
+    h->buf[kIterT] = spare;
+    rc = h->step(cur, t, nxt, &acc, &r, &upd);
+    if (rc) break;
+    t += r.tau_used;
+    if (results) results[k] = r;
+    s.steps += 1;
+    s.halvings += r.halvings;
+    s.radial_iterations += r.radial.iterations;
+    s.axial_iterations += r.axial.iterations;
+    s.cell_updates += upd;
+    s.cell_updates_accepted +=
+        static_cast<double>(h->active) * (r.radial.iterations + r.axial.iterations);
+    s.attempt_cells += 2.0 * static_cast<double>(h->active) * (r.halvings + 1);
+    // The accepted buffer becomes the field; the old field becomes scratch.
+    double* accepted = const_cast<double*>(acc);
+    double* old = cur;
+    cur = accepted;
+    if (accepted == nxt) {
+      nxt = old;
+    } else {
+      spare = old;
+    }
+  }
+  h->buf[kField] = cur;
+  h->buf[kNext] = nxt;
+  h->buf[kIterT] = spare;
+  CK(cudaMemcpyAsync(field, cur, sizeof(double) * h->cells(), cudaMemcpyDeviceToDevice,
+                     h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  GUARD_END(h)
+  s.t_end = t;
+  if (stats) *stats = s;
+  return rc;
+}
+
+int pcgpu_step_host(pcgpu_stepper* h, double* field_host, double t, pcgpu_step_result* r) {
+  if (!h || !field_host) return PCGPU_ERR_ARG;
+  GUARD_BEGIN
+  double* f = h->buf[kField];
+  CK(cudaMemcpyAsync(f, field_host, sizeof(double) * h->cells(), cudaMemcpyHostToDevice,
+                     h->stream));
+  const int rc = pcgpu_step(h, f, t, r);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(field_host, f, sizeof(double) * h->cells(), cudaMemcpyDeviceToHost,
+                     h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  GUARD_END(h)
+  return PCGPU_OK;
+}
+
+static int half_host(pcgpu_stepper* h, bool radial, const double* in_host, double t, double tau,
+                     double* out_host, pcgpu_outcome* o) {
+  GUARD_BEGIN
+  double* in = h->buf[kField];
+  double* out = h->buf[kNext];
+  CK(cudaMemcpyAsync(in, in_host, sizeof(double) * h->cells(), cudaMemcpyHostToDevice,
+                     h->stream));
+  CK(cudaMemcpyAsync(out, out_host, sizeof(double) * h->cells(), cudaMemcpyHostToDevice,
+                     h->stream));
+  const int rc = radial ? pcgpu_radial_half_step(h, in, t, tau, out, o)
+                        : pcgpu_axial_half_step(h, in, t, tau, out, o);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(out_host, out, sizeof(double) * h->cells(), cudaMemcpyDeviceToHost,
+                     h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  GUARD_END(h)
+  return PCGPU_OK;
+}
+
+int pcgpu_radial_half_step_host(pcgpu_stepper* h, const double* T_cur_host, double t,
+                                double tau, double* out_host, pcgpu_outcome* o) {
+  if (!h || !T_cur_host || !out_host || !o) return PCGPU_ERR_ARG;
+  return half_host(h, true, T_cur_host, t, tau, out_host, o);
+}
+
+int pcgpu_axial_half_step_host(pcgpu_stepper* h, const double* T_half_host, double t,
+                               double tau, double* out_host, pcgpu_outcome* o) {
+  if (!h || !T_half_host || !out_host || !o) return PCGPU_ERR_ARG;
+  return half_host(h, false, T_half_host, t, tau, out_host, o);
+}
+
+int pcgpu_clamp_events(const pcgpu_stepper* h, uint64_t* counts) {
+  if (!h || !counts) return PCGPU_ERR_ARG;
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) return PCGPU_ERR_CUDA;
+  if (cudaMemcpy(counts, h->P.clamp, sizeof(uint64_t) * h->d.n_layers, cudaMemcpyDeviceToHost) !=
+      cudaSuccess)
+    return PCGPU_ERR_CUDA;
+  return PCGPU_OK;
+}
+
+int pcgpu_enable_kernel_timing(pcgpu_stepper* h, int32_t on) {
+  h->timing = on != 0;
+  h->radial_ms = h->axial_ms = 0;
+  h->radial_launches = h->axial_launches = 0;
+  return PCGPU_OK;
+}
+
+int pcgpu_kernel_timing(const pcgpu_stepper* h, double* radial_ms, int64_t* radial_launches,
+                        double* axial_ms, int64_t* axial_launches) {
+  *radial_ms = h->radial_ms;
+  *radial_launches = h->radial_launches;
+  *axial_ms = h->axial_ms;
+  *axial_launches = h->axial_launches;
+  return PCGPU_OK;
+}
+
+}  // extern "C"

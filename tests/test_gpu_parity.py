@@ -1,0 +1,275 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Exact mode must be BIT-IDENTICAL to the reference (fields, tau sequence,
+Picard iteration counts, last_delta, clamp counts, error lines). The oracle is
+the C restatement (pinned to the reference itself by test_oracle_pin.py and to
+the committed fixtures by test_golden.py).
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle.oracle import OracleError, PortStepper, port_thomas_batch
+from paper_1912_03744_b200 import configs
+from paper_1912_03744_b200.errors import LineError, TableRangeError, TauFloorError
+from paper_1912_03744_b200.materials import HalfPointRule, RangePolicy
+from paper_1912_03744_b200.solver import make_field
+from paper_1912_03744_b200.source import FieldSource, NullSource
+
+from helpers import gpu_stepper, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _golden_cases():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("make_golden", os.path.join(GOLD, "make_golden.py"))
+    mg = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mg)
+    return mg.CASES
+
+
+def _seq(results):
+    return np.array([[r.tau_used, r.halvings, r.radial.iterations, r.axial.iterations,
+                      r.radial.last_delta, r.axial.last_delta] for r in results])
+
+
+@pytest.mark.parametrize("case_def", _golden_cases(), ids=lambda c: c[0])
+def test_exact_matches_golden_bitwise(cuda, case_def):
+    name, build, init, steps, t0 = case_def
+    z = np.load(os.path.join(GOLD, f"{name}.npz"))
+    case = build()
+    gpu = gpu_stepper(case, "exact")
+    f = to_dev(np.asfortranarray(z["initial"]))
+    t_end, stats, res = gpu.run(f, float(z["t0"]), int(z["steps"]), keep_results=True)
+    assert np.array_equal(_seq(res), z["seq"])
+    assert t_end == float(z["t_end"])
+    m = case.grid().mask()
+    assert np.array_equal(to_host(f)[m], z["final"][m])
+    assert gpu.clamp_events() == [int(v) for v in z["clamp"]]
+
+
+def test_exact_cfg0_2000_steps_bitwise(cuda):
+    """configs[0] in full: 100 x 200, tau = 1e-4, 2000 steps."""
+    case = configs.cfg0(2000)
+    g = case.grid()
+    port = PortStepper(case)
+    fo = make_field(g, case.solver.T0)
+    te_o, st_o, res_o = port.run(fo, 0.0, case.steps)
+    gpu = gpu_stepper(case, "exact")
+    fg = to_dev(make_field(g, case.solver.T0))
+    te_g, st_g, res_g = gpu.run(fg, 0.0, case.steps, keep_results=True)
+    assert te_g == te_o
+    assert np.array_equal(_seq(res_g), _seq(res_o))
+    m = g.mask()
+    assert np.array_equal(to_host(fg)[m], fo[m])
+    assert float(fo[m].max()) > 5.0  # the pulse heated the cell (~5.4 K)
+
+
+@pytest.mark.parametrize("rule", list(HalfPointRule))
+@pytest.mark.parametrize("api", ["device", "host"])
+def test_exact_half_steps_bitwise(cuda, rule, api):
+    case = configs.step_cell(True, halfpoint_rule=rule)
+    g = case.grid()
+    port, gpu = PortStepper(case), gpu_stepper(case, "exact")
+    f = configs.smooth_field(g, 30.0)
+    for tau in (2e-3, 5e-2):
+        ho = make_field(g, 0.0)
+        r_o = port.radial_half_step(f, 0.0, tau, ho)
+        if api == "host":
+            hg = make_field(g, 0.0)
+            r_g = gpu.radial_half_step(f, 0.0, tau, hg)
+        else:
+            hgd = to_dev(make_field(g, 0.0))
+            r_g = gpu.radial_half_step(to_dev(f), 0.0, tau, hgd)
+            hg = to_host(hgd)
+        assert r_g == r_o
+        m = g.mask()
+        assert np.array_equal(hg[m], ho[m])
+        no = make_field(g, 0.0)
+        a_o = port.axial_half_step(ho, 0.0, tau, no)
+        if api == "host":
+            ng = make_field(g, 0.0)
+            a_g = gpu.axial_half_step(ho, 0.0, tau, ng)
+        else:
+            ngd = to_dev(make_field(g, 0.0))
+            a_g = gpu.axial_half_step(to_dev(ho), 0.0, tau, ngd)
+            ng = to_host(ngd)
+        assert a_g == a_o
+        assert np.array_equal(ng[m], no[m])
+
+
+def test_equilibrium_one_iteration(cuda):
+    """test_solver.cpp:217-244."""
+    case = configs.step_cell(True, source=configs.SOURCE_NULL)
+    g = case.grid()
+    gpu = gpu_stepper(case, "exact", NullSource())
+    f = make_field(g, case.solver.T0)
+    out = make_field(g, 0.0)
+    r = gpu.radial_half_step(f, 0.0, 1e-3, out)
+    assert r.converged and r.iterations == 1
+    assert np.abs(out[g.mask()] - 4.2).max() <= 1e-13
+    out2 = make_field(g, 0.0)
+    r2 = gpu.axial_half_step(out, 0.0, 1e-3, out2)
+    assert r2.converged and r2.iterations == 1
+    assert np.abs(out2[g.mask()] - 4.2).max() <= 1e-13
+
+
+def test_constant_coefficients_two_iterations_exact_zero(cuda):
+    """test_solver.cpp:246-266: identical rebuilt system, identical solve."""
+    case = configs.step_cell(False, source=configs.SOURCE_NULL)
+    g = case.grid()
+    gpu = gpu_stepper(case, "exact", NullSource())
+    f = configs.smooth_field(g)
+    out = make_field(g, 0.0)
+    r = gpu.radial_half_step(f, 0.0, 2e-3, out)
+    assert r.converged and r.iterations == 2 and r.last_delta == 0.0
+    out2 = make_field(g, 0.0)
+    r2 = gpu.axial_half_step(out, 0.0, 2e-3, out2)
+    assert r2.converged and r2.iterations == 2 and r2.last_delta == 0.0
+
+
+def test_max_iter_one_forces_halving(cuda):
+    """test_solver.cpp:319-338."""
+    case = configs.step_cell(True, max_iter=1)
+    g = case.grid()
+    gpu = gpu_stepper(case, "exact")
+    f = to_dev(configs.smooth_field(g, 20.0))
+    t = 0.001
+    tau0 = gpu.initial_tau(t)
+    r = gpu.step(f, t)
+    assert r.halvings >= 1
+    assert r.tau_used == tau0 / 2 ** r.halvings
+    assert r.radial.converged and r.axial.converged
+
+
+def test_tau_floor_raises(cuda):
+    """test_solver.cpp:340-352."""
+    case = configs.step_cell(True, max_iter=1)
+    case.solver.tau_min = 0.9 * 1e-7
+    gpu = gpu_stepper(case, "exact")
+    with pytest.raises(TauFloorError):
+        gpu.step(to_dev(configs.smooth_field(case.grid(), 20.0)), 0.001)
+
+
+def test_strict_range_lowest_line(cuda):
+    case = configs.step_cell(True, range_policy=RangePolicy.Strict)
+    g = case.grid()
+    f = configs.smooth_field(g)
+    f[3, 5] = 500.0
+    f[9, 2] = 600.0
+    port, gpu = PortStepper(case), gpu_stepper(case, "exact")
+    with pytest.raises(OracleError) as eo:
+        port.radial_half_step(f, 0.0, 1e-3, make_field(g, 0.0))
+    with pytest.raises(LineError) as eg:
+        gpu.radial_half_step(f, 0.0, 1e-3, make_field(g, 0.0))
+    assert eg.value.cause is TableRangeError
+    assert eg.value.line == eo.value.line
+
+
+def _heat_sum(case, f):
+    """weighted_heat_sum (solver.cpp:103-119), Kahan-summed."""
+    g = case.grid()
+    s = comp = 0.0
+    for i in range(g.nr()):
+        mat = case.materials[g.layer(i)]
+        for j in range(g.col_extent(i)):
+            cv = mat.cv(f[i, j])
+            term = g.r_center(i) * g.control_r(i) * g.control_z(j) * mat.rho() * cv * f[i, j]
+            y = term - comp
+            t = s + y
+            comp = (t - s) - y
+            s = t
+    return s
+
+
+def test_conservation_all_neumann(cuda):
+    """test_solver.cpp:354-369: source-free heat is conserved."""
+    case = configs.step_cell(False, source=configs.SOURCE_NULL, all_neumann=True)
+    gpu = gpu_stepper(case, "exact", NullSource())
+    f = configs.smooth_field(case.grid(), 12.0)
+    before = _heat_sum(case, f)
+    fd = to_dev(f)
+    t = 0.0
+    for _ in range(30):
+        t += gpu.step(fd, t).tau_used
+    after = _heat_sum(case, to_host(fd))
+    assert abs(after - before) / abs(before) <= 1e-11
+
+
+def test_z_independence(cuda):
+    """test_solver.cpp:433-468."""
+    case = configs.step_cell(True, source=configs.SOURCE_NULL, all_neumann=True)
+    case.domain.outer_length = case.domain.core_length
+    g = case.grid()
+    gpu = gpu_stepper(case, "exact", NullSource())
+    f = make_field(g, 4.2)
+    for i in range(g.nr()):
+        f[i, :] = 5.0 + math.cos(2.0 * g.r_center(i))
+    fd = to_dev(f)
+    t = 0.0
+    for _ in range(20):
+        t += gpu.step(fd, t).tau_used
+    h = to_host(fd)
+    assert np.abs(h - h[:, :1]).max() <= 1e-12
+
+
+class _Manufactured(FieldSource):
+    """T-independent per-cell power (the acceptance suite's MMS pattern)."""
+
+    def power_field(self, grid, t):
+        r = grid.r_centers[:, None]
+        z = grid.z_centers[None, :]
+        return np.asfortranarray(1e3 * np.exp(-5 * t) * np.cos(np.pi * r * r) * np.cos(0.5 * np.pi * z)
+                                 + 0 * r * z)
+
+
+def test_field_source_half_steps_bitwise(cuda):
+    case = configs.step_cell(True, source=configs.SOURCE_FIELD)
+    g = case.grid()
+    src = _Manufactured(g)
+    gpu = gpu_stepper(case, "exact", src)
+    port = PortStepper(case)
+    f = configs.smooth_field(g, 10.0)
+    t, tau = 0.01, 1e-3
+    port.bind_power_field(src.power_field(g, t + 0.5 * tau))
+    ho, hg = make_field(g, 0.0), make_field(g, 0.0)
+    assert gpu.radial_half_step(f, t, tau, hg) == port.radial_half_step(f, t, tau, ho)
+    assert np.array_equal(hg[g.mask()], ho[g.mask()])
+    no, ng = make_field(g, 0.0), make_field(g, 0.0)
+    assert gpu.axial_half_step(ho, t, tau, ng) == port.axial_half_step(ho, t, tau, no)
+    assert np.array_equal(ng[g.mask()], no[g.mask()])
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+def test_tridiag_batch_exact_bitwise(cuda, layout):
+    import torch
+    from paper_1912_03744_b200.tridiagonal import thomas_solve_batch
+    z = np.load(os.path.join(GOLD, "thomas_batch.npz"))
+    batch, n = z["x"].shape
+    if layout == 0:
+        host = [np.ascontiguousarray(z[k].reshape(-1)) for k in ("lower", "diag", "upper", "rhs")]
+    else:
+        host = [np.ascontiguousarray(z[k].T.reshape(-1)) for k in ("lower", "diag", "upper", "rhs")]
+    dev = [torch.from_numpy(h).cuda() for h in host]
+    x = torch.empty_like(dev[3])
+    thomas_solve_batch(*dev, x, n, batch, layout, exact=True)
+    got = x.cpu().numpy()
+    want = z["x"].reshape(-1) if layout == 0 else np.ascontiguousarray(z["x"].T).reshape(-1)
+    assert np.array_equal(got, want)
+
+
+def test_tridiag_batch_zero_pivot(cuda):
+    import torch
+    from paper_1912_03744_b200.tridiagonal import thomas_solve_batch
+    n, batch = 5, 8
+    b = torch.ones(n * batch, dtype=torch.float64, device="cuda")
+    b[3 * n + 2] = 0.0
+    b[6 * n] = 0.0
+    z = torch.zeros_like(b)
+    with pytest.raises(LineError) as e:
+        thomas_solve_batch(z, b, z, torch.ones_like(b), torch.empty_like(b), n, batch, 0)
+    assert e.value.line == 3
