@@ -38,19 +38,23 @@ void launch_axial_exact(const DevProblem& P, int it, double eps, const double* T
 void launch_transpose_N2T(const DevProblem& P, const double* srcN, double* dstT, cudaStream_t s);
 void launch_transpose_T2N(const DevProblem& P, const double* srcT, double* dstN, cudaStream_t s);
 
-// ---- fast mode (adi_fast.cu) ----
+// ---- fast mode (adi_fast.cu): partitioned line solves on contiguous lines ----
 bool fast_supported(const DevProblem& P);
+// K3: explN = Lambda_z[field] and TcN = field (from the T-layout field).
+void launch_explicit_axial_fast(const DevProblem& P, const double* fieldT, double* explN,
+                                double* TcN, DevStatus* st, cudaStream_t s);
+// K1: radial Picard iteration on N-layout lines.
 void launch_radial_fast(const DevProblem& P, int it, double eps, double half_k, double pulse,
                         const double* TsN, const double* TcN, const double* explN,
                         const double* powN, double* outN, DevStatus* st, cudaStream_t s);
-void launch_explicit_axial_fast(const DevProblem& P, const double* srcN, double* explN,
-                                DevStatus* st, cudaStream_t s);
-void launch_axial_rhs_fast(const DevProblem& P, double half_k, double pulse, const double* halfN,
-                           const double* powN, double* kbarT, double* explT, double* halfT,
-                           DevStatus* st, cudaStream_t s);
-void launch_axial_fast(const DevProblem& P, int it, double eps, const double* TsT,
-                       const double* ThT, const double* kbarT, const double* explT,
-                       double* outT, DevStatus* st, cudaStream_t s);
+// K4: explT = Lambda_r[half] + X(half) and halfT = half (from the N-layout half field).
+void launch_axial_rhs_fast(const DevProblem& P, double pulse, const double* halfN,
+                           const double* powN, double* explT, double* halfT, DevStatus* st,
+                           cudaStream_t s);
+// K2: axial Picard iteration on T-layout lines (K-bar recomputed from the anchor).
+void launch_axial_fast(const DevProblem& P, int it, double eps, double half_k, const double* TsT,
+                       const double* ThT, const double* explT, double* outT, DevStatus* st,
+                       cudaStream_t s);
 
 // Kernel launch counter (for the bench's gpu_launches claim).
 extern unsigned long long g_launches;

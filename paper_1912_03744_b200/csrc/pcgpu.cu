@@ -121,6 +121,8 @@ std::string validate(const pcgpu_desc* d) {
     return "source: unknown kind";
   }
   if (d->mode != PCGPU_MODE_EXACT && d->mode != PCGPU_MODE_FAST) return "pcgpu: unknown mode";
+  if (d->mode == PCGPU_MODE_FAST && (d->nr > 16384 || d->nz > 16384))
+    return "pcgpu: fast mode supports lines of up to 16384 cells";
   return "";
 }
 
@@ -309,83 +311,88 @@ struct pcgpu_stepper {
     return 0;
   }
 
-  // Radial half-step from an N-layout anchor. On success *resT points at the
-  // T-layout result buffer (exact mode) / N-layout (fast mode).
-  int radial(const double* TcN, double t, double tau, const double** res, pcgpu_outcome* o) {
+  // State layout of the field between steps: N in exact mode (the radial
+  // sweep's explicit pass reads N and writes the T copies it needs), T in fast
+  // mode (the axial sweep's output layout; the radial explicit pass reads T).
+  bool fast() const { return d.mode == PCGPU_MODE_FAST; }
+
+  // Radial half-step from the anchor `field` (state layout). On success *res
+  // points at the result: T layout (exact) / N layout (fast).
+  int radial(const double* field, double t, double tau, const double** res, pcgpu_outcome* o) {
     const double pulse = pulse_for(t, tau);
     const double hk = 2.0 / tau;
     reset_status();
-    if (d.mode == PCGPU_MODE_EXACT) {
-      launch_explicit_axial_exact(P, TcN, buf[kExpl], buf[kTcT], st, stream);
-      auto src_of = [&](int it) -> const double* {
-        return it == 1 ? buf[kTcT] : (it % 2 == 0 ? buf[kHalfT] : buf[kIterT]);
-      };
-      auto dst_of = [&](int it) -> double* { return it % 2 == 1 ? buf[kHalfT] : buf[kIterT]; };
-      const int conv = picard(0, pred_radial, [&](int it) {
+    auto dst_of = [&](int it) -> double* { return it % 2 == 1 ? buf[kHalfT] : buf[kIterT]; };
+    auto src_of = [&](int it) -> const double* {
+      return it == 1 ? buf[kTcT] : (it % 2 == 0 ? buf[kHalfT] : buf[kIterT]);
+    };
+    int conv;
+    if (!fast()) {
+      launch_explicit_axial_exact(P, field, buf[kExpl], buf[kTcT], st, stream);
+      conv = picard(0, pred_radial, [&](int it) {
         launch_radial_exact(P, it, d.epsilon, hk, pulse, src_of(it), buf[kTcT], buf[kExpl],
                             buf[kPowT], dst_of(it), buf[kW], buf[kX], st, stream);
       }, o);
-      if (conv < 0) return -conv;
-      if (conv > 0) *res = dst_of(conv);
-      return PCGPU_OK;
+    } else {
+      launch_explicit_axial_fast(P, field, buf[kExpl], buf[kTcT], st, stream);
+      conv = picard(0, pred_radial, [&](int it) {
+        launch_radial_fast(P, it, d.epsilon, hk, pulse, src_of(it), buf[kTcT], buf[kExpl],
+                           buf[kPowN], dst_of(it), st, stream);
+      }, o);
     }
-    // fast mode: N layout throughout the radial sweep.
-    launch_explicit_axial_fast(P, TcN, buf[kExpl], st, stream);
-    auto src_of = [&](int it) -> const double* {
-      return it == 1 ? TcN : (it % 2 == 0 ? buf[kHalfT] : buf[kIterT]);
-    };
-    auto dst_of = [&](int it) -> double* { return it % 2 == 1 ? buf[kHalfT] : buf[kIterT]; };
-    const int conv = picard(0, pred_radial, [&](int it) {
-      launch_radial_fast(P, it, d.epsilon, hk, pulse, src_of(it), TcN, buf[kExpl], buf[kPowN],
-                         dst_of(it), st, stream);
-    }, o);
     if (conv < 0) return -conv;
     if (conv > 0) *res = dst_of(conv);
     return PCGPU_OK;
   }
 
-  // Axial half-step from the radial result (layout per mode). `out` (N) is
-  // the preferred destination; *res receives the N-layout buffer holding the
-  // result (out or the ping-pong buffer).
+  // Axial half-step from the radial result `half` (T layout in exact mode, N
+  // in fast mode). `out` (state layout) is the preferred destination; *res
+  // receives the state-layout buffer holding the result (out or the
+  // ping-pong buffer).
   int axial(const double* half, double t, double tau, double* out, const double** res,
             pcgpu_outcome* o) {
     const double pulse = pulse_for(t, tau);
     const double hk = 2.0 / tau;
     reset_status();
-    if (d.mode == PCGPU_MODE_EXACT) {
-      double* halfN = buf[kTcT];
-      launch_axial_rhs_exact(P, hk, pulse, half, buf[kPowN], buf[kKbar], buf[kExpl], halfN, st,
+    double* anchor = buf[kTcT];  // halfN (exact) / halfT (fast)
+    auto src_of = [&](int it) -> const double* {
+      return it == 1 ? anchor : (it % 2 == 0 ? out : buf[kIterT]);
+    };
+    auto dst_of = [&](int it) -> double* { return it % 2 == 1 ? out : buf[kIterT]; };
+    int conv;
+    if (!fast()) {
+      launch_axial_rhs_exact(P, hk, pulse, half, buf[kPowN], buf[kKbar], buf[kExpl], anchor, st,
                              stream);
-      auto src_of = [&](int it) -> const double* {
-        return it == 1 ? halfN : (it % 2 == 0 ? out : buf[kIterT]);
-      };
-      auto dst_of = [&](int it) -> double* { return it % 2 == 1 ? out : buf[kIterT]; };
-      const int conv = picard(1, pred_axial, [&](int it) {
-        launch_axial_exact(P, it, d.epsilon, src_of(it), halfN, buf[kKbar], buf[kExpl],
+      conv = picard(1, pred_axial, [&](int it) {
+        launch_axial_exact(P, it, d.epsilon, src_of(it), anchor, buf[kKbar], buf[kExpl],
                            dst_of(it), buf[kW], buf[kX], st, stream);
       }, o);
-      if (conv < 0) return -conv;
-      if (conv > 0) *res = dst_of(conv);
-      return PCGPU_OK;
-    }
-    // fast mode: the z-sweep runs on the T layout; results transposed back.
-    double* halfT = buf[kTcT];
-    launch_axial_rhs_fast(P, hk, pulse, half, buf[kPowN], buf[kKbar], buf[kExpl], halfT, st,
+    } else {
+      launch_axial_rhs_fast(P, pulse, half, buf[kPowN], buf[kExpl], anchor, st, stream);
+      conv = picard(1, pred_axial, [&](int it) {
+        launch_axial_fast(P, it, d.epsilon, hk, src_of(it), anchor, buf[kExpl], dst_of(it), st,
                           stream);
-    auto src_of = [&](int it) -> const double* {
-      return it == 1 ? halfT : (it % 2 == 0 ? buf[kX] : buf[kIterT]);
-    };
-    auto dst_of = [&](int it) -> double* { return it % 2 == 1 ? buf[kX] : buf[kIterT]; };
-    const int conv = picard(1, pred_axial, [&](int it) {
-      launch_axial_fast(P, it, d.epsilon, src_of(it), halfT, buf[kKbar], buf[kExpl],
-                        dst_of(it), st, stream);
-    }, o);
-    if (conv < 0) return -conv;
-    if (conv > 0) {
-      launch_transpose_T2N(P, dst_of(conv), out, stream);
-      *res = out;
+      }, o);
     }
+    if (conv < 0) return -conv;
+    if (conv > 0) *res = dst_of(conv);
     return PCGPU_OK;
+  }
+
+  // N-layout user field <-> state layout.
+  void to_state(const double* fieldN, double* state) {
+    if (fast())
+      launch_transpose_N2T(P, fieldN, state, stream);
+    else
+      CK(cudaMemcpyAsync(state, fieldN, sizeof(double) * cells(), cudaMemcpyDeviceToDevice,
+                         stream));
+  }
+  void from_state(const double* state, double* fieldN) {
+    if (fast())
+      launch_transpose_T2N(P, state, fieldN, stream);
+    else if (state != fieldN)
+      CK(cudaMemcpyAsync(fieldN, state, sizeof(double) * cells(), cudaMemcpyDeviceToDevice,
+                         stream));
   }
 
   // step(): tau controller (solver.cpp:356-373). `field` is N layout; on
@@ -479,7 +486,7 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
     std::vector<int> layer(d->layer, d->layer + nr);
 
     // Tables, flattened.
-    std::vector<double> knots, vals;
+    std::vector<double> knots, vals, slopes;
     DevProblem& P = h->P;
     P.n_layers = d->n_layers;
     for (int m = 0; m < d->n_layers; ++m) {
@@ -495,6 +502,7 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
         for (int k = 0; k < t.n; ++k) {
           knots.push_back(t.t[k]);
           vals.push_back(t.v[k]);
+          slopes.push_back(k == 0 ? 0.0 : (t.v[k] - t.v[k - 1]) / (t.t[k] - t.t[k - 1]));
         }
         if (t.n >= 3) {
           // Uniform-knot bracket guess (exactness is kept by the device fix-up).
@@ -531,6 +539,7 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
     P.width_z = up(width_z);
     P.knots = up(knots);
     P.vals = up(vals);
+    P.slopes = up(slopes);
     P.source_kind = d->source_kind;
     P.source_layer = d->source_layer;
     P.amplitude = d->amplitude;
@@ -555,6 +564,7 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
     std::vector<double> t0fill(h->cells(), d->T0);
     for (int b = 0; b < kNumBufs; ++b) {
       if ((b == kPowN || b == kPowT) && d->source_kind != PCGPU_SOURCE_FIELD) continue;
+      if ((b == kW || b == kKbar) && d->mode == PCGPU_MODE_FAST) continue;  // exact-mode only
       double* p = nullptr;
       CK(cudaMalloc(&p, bytes));
       h->dev_allocs.push_back(p);
@@ -603,11 +613,16 @@ int pcgpu_radial_half_step(pcgpu_stepper* h, const double* T_cur, double t, doub
                            double* out, pcgpu_outcome* o) {
   if (!h || !T_cur || !out || !o || out == T_cur) return PCGPU_ERR_ARG;
   GUARD_BEGIN
+  const double* anchor = T_cur;
+  if (h->fast()) {
+    launch_transpose_N2T(h->P, T_cur, h->buf[kX], h->stream);
+    anchor = h->buf[kX];
+  }
   const double* res = nullptr;
-  const int rc = h->radial(T_cur, t, tau, &res, o);
+  const int rc = h->radial(anchor, t, tau, &res, o);
   if (rc) return rc;
   if (o->converged) {
-    if (h->d.mode == PCGPU_MODE_EXACT)
+    if (!h->fast())
       launch_transpose_T2N(h->P, res, out, h->stream);
     else
       CK(cudaMemcpyAsync(out, res, sizeof(double) * h->cells(), cudaMemcpyDeviceToDevice,
@@ -623,16 +638,15 @@ int pcgpu_axial_half_step(pcgpu_stepper* h, const double* T_half, double t, doub
   if (!h || !T_half || !out || !o || out == T_half) return PCGPU_ERR_ARG;
   GUARD_BEGIN
   const double* half = T_half;
-  if (h->d.mode == PCGPU_MODE_EXACT) {
+  if (!h->fast()) {
     launch_transpose_N2T(h->P, T_half, h->buf[kHalfT], h->stream);
     half = h->buf[kHalfT];
   }
+  double* dst = h->fast() ? h->buf[kNext] : out;
   const double* res = nullptr;
-  const int rc = h->axial(half, t, tau, out, &res, o);
+  const int rc = h->axial(half, t, tau, dst, &res, o);
   if (rc) return rc;
-  if (o->converged && res != out)
-    CK(cudaMemcpyAsync(out, res, sizeof(double) * h->cells(), cudaMemcpyDeviceToDevice,
-                       h->stream));
+  if (o->converged) h->from_state(res, out);
   CK(cudaStreamSynchronize(h->stream));
   GUARD_END(h)
   return PCGPU_OK;
@@ -643,11 +657,15 @@ int pcgpu_step(pcgpu_stepper* h, double* field, double t, pcgpu_step_result* r) 
   GUARD_BEGIN
   const double* acc = nullptr;
   double upd = 0;
-  const int rc = h->step(field, t, h->buf[kNext], &acc, r, &upd);
+  const double* state = field;
+  if (h->fast()) {
+    h->to_state(field, h->buf[kField]);
+    state = h->buf[kField];
+  }
+  const int rc = h->step(state, t, h->buf[kNext], &acc, r, &upd);
   if (rc) return rc;
   // field.swap(next_) (solver.cpp:364): the caller's array receives the result.
-  CK(cudaMemcpyAsync(field, acc, sizeof(double) * h->cells(), cudaMemcpyDeviceToDevice,
-                     h->stream));
+  h->from_state(acc, field);
   CK(cudaStreamSynchronize(h->stream));
   GUARD_END(h)
   return PCGPU_OK;
@@ -664,8 +682,7 @@ int pcgpu_run(pcgpu_stepper* h, double* field, double t0, int32_t nsteps,
   double* cur = h->buf[kField];
   double* nxt = h->buf[kNext];
   double* spare = h->buf[kIterT];
-  CK(cudaMemcpyAsync(cur, field, sizeof(double) * h->cells(), cudaMemcpyDeviceToDevice,
-                     h->stream));
+  h->to_state(field, cur);
   for (int32_t k = 0; k < nsteps; ++k) {
     pcgpu_step_result r;
     const double* acc = nullptr;
@@ -696,8 +713,7 @@ int pcgpu_run(pcgpu_stepper* h, double* field, double t0, int32_t nsteps,
   h->buf[kField] = cur;
   h->buf[kNext] = nxt;
   h->buf[kIterT] = spare;
-  CK(cudaMemcpyAsync(field, cur, sizeof(double) * h->cells(), cudaMemcpyDeviceToDevice,
-                     h->stream));
+  h->from_state(cur, field);
   CK(cudaStreamSynchronize(h->stream));
   GUARD_END(h)
   s.t_end = t;
