@@ -31,6 +31,8 @@
 #include <cooperative_groups.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <type_traits>
 
 #include "adi_kernels.h"
 
@@ -81,21 +83,61 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
-struct Tile {
+struct alignas(16) Tile {
   double v[SEG];
 };
 
 struct FastSmem {
-  Tile ts, ta, ex;             // iterate, anchor, explicit term (swizzled)
+  // small per-CTA state first (low shared-memory offsets)
   double halo[4];              // ts[seg0-1], ta[seg0-1], ts[seg0+SEG], ta[seg0+SEG]
-  double fu[NT + 1], fv[NT + 1], fw[NT + 1];  // first-interior-row affine forms
-  double pL[2][NT], pD[2][NT], pU[2][NT], pY[2][NT], pP[2][NT], pR[2][NT];  // PCR
-  double q[NT];                // reduced unknowns (last row of each chunk)
   double bnd[kMaxCluster][6];  // per-CTA boundary forms (y0,p0,r0,yL,pL,rL)
   double EF[2];                // E_{rank-1}, F_{rank+1}
   double bs[4][kMaxCluster + 1];  // boundary-system scratch (ph, ps, ea, eb)
-  double wmax[NT / 32];
+  double fu[NT + 1], fv[NT + 1], fw[NT + 1];  // first-interior-row affine forms
+  double q[NT];                // reduced unknowns (last row of each chunk)
+  double pL[2][NT], pD[2][NT], pU[2][NT], pY[2][NT], pP[2][NT], pR[2][NT];  // PCR
+  Tile ts, ta, ex;             // iterate, anchor, explicit term (swizzled, 16-B aligned)
 };
+
+// Lean-variant table lookup (all tables of a property share an exactly
+// uniform power-of-two knot grid): clamp by selects, bracket by arithmetic,
+// interval start recomputed exactly (t0 + (k-1) h), one 16-B load {v, slope}.
+// Returns the value and counts an out-of-range evaluation in *oor.
+// Reciprocal without the IEEE slow path: MUFU seed + two Newton steps
+// (relative error ~1 ulp for the normal, positive pivots of these M-matrices).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = __fma_rn(-x, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-x, r, 1.0);
+  return __fma_rn(r, e, r);
+}
+
+// Register-resident per-layer table data for the lean lookup.
+struct LeanTab {
+  int off;
+  double v0, vK;
+};
+
+// Lean-variant lookup. Tables of one property share an exactly uniform
+// power-of-two knot grid across layers (P.lean_*); entry (prop, layer, k) of
+// P.lean_tab holds {v[k-1], slope_k}. T is clamped to the knot range first;
+// at the clamp points the interpolation reproduces the end values up to one
+// rounding. Out-of-range evaluations (clamp_events) are counted in `oor`.
+__device__ __forceinline__ double lean_lookup2(const DevProblem& P, int prop, int L, double T,
+                                               int& oor, bool valid) {
+  const double t0 = P.lean_t0[prop], tK = P.lean_tK[prop];
+  const double Tc = fmin(fmax(T, t0), tK);
+  int k = static_cast<int>(__dmul_rn(Tc - t0, P.lean_inv_h[prop])) + 1;
+  k = min(k, P.lean_kmax[prop]);
+  const double2 vs =
+      __ldg(reinterpret_cast<const double2*>(P.lean_tab) + P.lean_base[prop] +
+            L * P.lean_stride[prop] + k);
+  const double tlo = __dadd_rn(t0, __dmul_rn(static_cast<double>(k - 1), P.lean_h[prop]));
+  oor += (valid && !(T >= t0 && T <= tK)) ? 1 : 0;
+  return __dadd_rn(vs.x, __dmul_rn(Tc - tlo, vs.y));
+}
 
 __device__ __forceinline__ double tile_get(const Tile& t, int e) {
   return *reinterpret_cast<const double*>(reinterpret_cast<const char*>(t.v) + swz(e));
@@ -103,6 +145,7 @@ __device__ __forceinline__ double tile_get(const Tile& t, int e) {
 __device__ __forceinline__ void tile_put(Tile& t, int e, double v) {
   *reinterpret_cast<double*>(reinterpret_cast<char*>(t.v) + swz(e)) = v;
 }
+
 struct LineArgs {
   const double* Ts;  // Picard iterate
   const double* Ta;  // anchor (T_cur for the radial sweep, T_half for the axial)
@@ -118,8 +161,12 @@ struct LineArgs {
 
 // ---------------------------------------------------------------------------
 // One Picard iteration of a sweep over contiguous lines.
-template <bool kAxial>
-__global__ void __launch_bounds__(NT) k_line_fast(DevProblem P, LineArgs A) {
+// kLean: 0 = generic (any rule / policy / table / source); 1 = lean, no
+// source term in the sweep; 2 = lean with the Joule source (radial sweep).
+// Lean requires: MeanTemperature faces, Clamp policy, every table exactly
+// uniform (power-of-two step) with one knot grid per property across layers.
+template <bool kAxial, bool kU2, int kLean>
+__global__ void __launch_bounds__(NT, 3) k_line_fast(DevProblem P, LineArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FastSmem& S = *reinterpret_cast<FastSmem*>(smem_raw);
   if (skip_iteration(A.st, A.it, A.eps)) return;
@@ -203,13 +250,13 @@ __global__ void __launch_bounds__(NT) k_line_fast(DevProblem P, LineArgs A) {
     c = 0.0;
     if (f >= 1 && f <= n - 1) {
       if (kAxial) {
-        const double lam = k == 0 ? face_lambda_fast<false>(P, Lline, Lline, ts_lo, ts_hi, A.st, line)
-                                  : face_lambda_fast(P, Lline, Lline, ts_lo, ts_hi, A.st, line);
+        const double lam = k == 0 ? face_lambda_fast<false, kU2>(P, Lline, Lline, ts_lo, ts_hi, A.st, line)
+                                  : face_lambda_fast<true, kU2>(P, Lline, Lline, ts_lo, ts_hi, A.st, line);
         c = lam * P.inv_gap_z[f];
       } else {
         const int lo = P.layer[f - 1], hi = P.layer[f];
-        const double lam = k == 0 ? face_lambda_fast<false>(P, lo, hi, ts_lo, ts_hi, A.st, line)
-                                  : face_lambda_fast(P, lo, hi, ts_lo, ts_hi, A.st, line);
+        const double lam = k == 0 ? face_lambda_fast<false, kU2>(P, lo, hi, ts_lo, ts_hi, A.st, line)
+                                  : face_lambda_fast<true, kU2>(P, lo, hi, ts_lo, ts_hi, A.st, line);
         c = P.face_r_lo[f] * lam * P.inv_gap_r[f];
       }
     }
@@ -220,7 +267,119 @@ __global__ void __launch_bounds__(NT) k_line_fast(DevProblem P, LineArgs A) {
   double cp[R - 1], up[R - 1], vp[R - 1];
   double wp = 0.0;
   double AL = 0.0, CL_ = 0.0, bL = 1.0, dL = 0.0;
-  {
+  if (kLean) {
+    // Branch-free assembly: invalid faces/rows are neutralised by selects;
+    // table data comes from the property-grouped lean table (one 16-B load
+    // per lookup, no per-row parameter indexing).
+    const int nm1 = n - 1;
+    const int Lax = kAxial ? P.layer[line] : 0;
+    const double rho_hk_ax = kAxial ? P.mats[Lax].rho * A.hk : 0.0;
+    const double src_amp = (kLean == 2 && A.pulse != 0.0) ? P.amplitude * A.pulse : 0.0;
+    int oor = 0;  // out-of-range evaluations (clamp_events), axial sweep
+    double ts_c = ld_ts(0), ta_c = ld_ta(0);
+    double fc_lo, fl_lo;
+    int Lc = kAxial ? Lax : __ldg(P.layer + min(s, P.nr - 1));
+    {
+      // face s (lower face of the chunk): owned by the previous chunk's count
+      const int f = s;
+      const bool vf = f >= 1 && f <= nm1;
+      const double tp = ld_ts(-1), tpa = ld_ta(-1);
+      int dummy = 0;
+      double c;
+      if (kAxial) {
+        c = lean_lookup2(P, kLambda, Lax, 0.5 * (tp + ts_c), dummy, false) *
+            __ldg(P.inv_gap_z + min(f, P.nz));
+      } else {
+        const int Lp = __ldg(P.layer + min(max(f - 1, 0), P.nr - 1));
+        c = lean_lookup2(P, kLambda, Lp, 0.5 * (tp + ts_c), dummy, false) *
+            __ldg(P.gfac_r + min(f, P.nr));
+      }
+      fc_lo = vf ? c : 0.0;
+      fl_lo = fc_lo * (ta_c - tpa);
+    }
+    double cp_prev = 0.0, up_prev = 0.0, vp_prev = 0.0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int i = s + k;
+      const double ts_n = ld_ts(k + 1), ta_n = ld_ta(k + 1);
+      const int f = i + 1;  // face between rows i and i+1
+      const bool vf = f <= nm1;
+      const bool vi = i < n;
+      int Ln = Lc;
+      double c;
+      if (kAxial) {
+        c = lean_lookup2(P, kLambda, Lax, 0.5 * (ts_c + ts_n), oor, vf) *
+            __ldg(P.inv_gap_z + min(f, P.nz));
+      } else {
+        Ln = __ldg(P.layer + min(f, P.nr - 1));
+        int o = 0;
+        c = lean_lookup2(P, kLambda, Lc, 0.5 * (ts_c + ts_n), o, vf) *
+            __ldg(P.gfac_r + min(f, P.nr));
+        if (o) atomicAdd(P.clamp + Lc, 1ull);
+      }
+      const double fc_hi = vf ? c : 0.0;
+      const double fl_hi = fc_hi * (ta_n - ta_c);
+      const double exk = tile_get(S.ex, e0 + k);
+      double Ak, Ck, bk, dk;
+      if (kAxial) {
+        const double inv_eta = __ldg(P.inv_eta + min(i, P.nz - 1));
+        Ak = fc_lo * inv_eta;
+        Ck = fc_hi * inv_eta;
+        const double K = rho_hk_ax * lean_lookup2(P, kCv, Lax, ta_c, oor, vi);
+        bk = K + Ak + Ck;
+        // terminal face: face_top is nonzero only on Dirichlet lines
+        const bool top = i == nm1;
+        bk += top ? face_top * inv_eta : 0.0;
+        const double fh = fl_hi + (top ? face_top * (P.T0 - ta_c) : 0.0);
+        dk = exk + (fh - fl_lo) * inv_eta;
+      } else {
+        const double inv_vol = __ldg(P.inv_vol_r + min(i, P.nr - 1));
+        Ak = fc_lo * inv_vol;
+        Ck = fc_hi * inv_vol;
+        int o = 0;
+        const double K = P.lean_rho[Lc] * A.hk * lean_lookup2(P, kCv, Lc, ts_c, o, vi);
+        double src = 0.0;
+        if (kLean == 2) {
+          // JouleSource::power: chi(T) * amplitude * pulse in the source layer
+          const bool on = Lc == P.source_layer;
+          src = (on ? src_amp : 0.0) *
+                lean_lookup2(P, kChi, P.source_layer, ts_c, o, vi && on && src_amp != 0.0);
+        }
+        if (o) atomicAdd(P.clamp + Lc, static_cast<unsigned long long>(o));
+        bk = K + Ak + Ck;
+        dk = (fl_hi - fl_lo) * inv_vol + exk + src;
+      }
+      Ak = vi ? Ak : 0.0;
+      Ck = vi ? Ck : 0.0;
+      bk = vi ? bk : 1.0;
+      dk = vi ? dk : 0.0;
+      if (k < R - 1) {
+        const double piv = k == 0 ? bk : bk + Ak * cp_prev;
+        const double ip = rcp_nr(piv);
+        const double cc = k < R - 2 ? -Ck * ip : 0.0;
+        if (k == R - 2) wp = Ck * ip;
+        const double u = k == 0 ? dk * ip : (dk + Ak * up_prev) * ip;
+        const double v = k == 0 ? Ak * ip : Ak * vp_prev * ip;
+        cp[k] = cc;
+        up[k] = u;
+        vp[k] = v;
+        cp_prev = cc;
+        up_prev = u;
+        vp_prev = v;
+      } else {
+        AL = Ak;
+        CL_ = Ck;
+        bL = bk;
+        dL = dk;
+      }
+      ts_c = ts_n;
+      ta_c = ta_n;
+      fc_lo = fc_hi;
+      fl_lo = fl_hi;
+      Lc = Ln;
+    }
+    if (kAxial && oor) atomicAdd(P.clamp + Lax, static_cast<unsigned long long>(oor));
+  } else {
     double ts_c = ld_ts(0), ta_c = ld_ta(0);
     double fc_lo, fl_lo;
     face(0, ld_ts(-1), ts_c, ld_ta(-1), ta_c, fc_lo, fl_lo);
@@ -238,7 +397,7 @@ __global__ void __launch_bounds__(NT) k_line_fast(DevProblem P, LineArgs A) {
           const double inv_eta = P.inv_eta[i];
           Ak = fc_lo * inv_eta;
           Ck = fc_hi * inv_eta;
-          const double K = rho_hk * mat_eval_fast(P, Lline, kCv, ta_c, A.st, line);
+          const double K = rho_hk * mat_eval_fast<true, kU2>(P, Lline, kCv, ta_c, A.st, line);
           bk = K + Ak + Ck;
           double fh = fl_hi;
           if (i == n - 1 && dirichlet) {
@@ -251,12 +410,12 @@ __global__ void __launch_bounds__(NT) k_line_fast(DevProblem P, LineArgs A) {
           const double inv_vol = P.inv_vol_r[i];
           Ak = fc_lo * inv_vol;
           Ck = fc_hi * inv_vol;
-          const double K = P.mats[L].rho * A.hk * mat_eval_fast(P, L, kCv, ts_c, A.st, line);
+          const double K = P.mats[L].rho * A.hk * mat_eval_fast<true, kU2>(P, L, kCv, ts_c, A.st, line);
           bk = K + Ak + Ck;
           const double fp = P.source_kind == PCGPU_SOURCE_FIELD
                                 ? A.pw[static_cast<size_t>(line) * P.nr + i] : 0.0;
           dk = (fl_hi - fl_lo) * inv_vol + exk +
-               source_power_fast(P, A.pulse, L, ts_c, fp, A.st, line);
+               source_power_fast<kU2>(P, A.pulse, L, ts_c, fp, A.st, line);
         }
       }
       if (k < R - 1) {
@@ -553,15 +712,19 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-template <bool kAxial>
-void launch_line(const DevProblem& P, const LineArgs& A, int nmax, cudaStream_t s) {
+void report_launch_error(cudaError_t e) {
+  // Surfaced to the host at the next synchronisation as a sticky error.
+  fprintf(stderr, "pcgpu: k_line_fast launch failed: %s\n", cudaGetErrorString(e));
+}
+
+template <bool kAxial, bool kU2, int kLean>
+void launch_line_t(const DevProblem& P, const LineArgs& A, int nmax, cudaStream_t s) {
   const int CL = (nmax + SEG - 1) / SEG;
   const size_t smem = sizeof(FastSmem);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_line_fast<kAxial>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    cudaFuncSetAttribute(k_line_fast<kAxial>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    cudaFuncSetAttribute(k_line_fast<kAxial, kU2, kLean>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -576,8 +739,23 @@ void launch_line(const DevProblem& P, const LineArgs& A, int nmax, cudaStream_t 
   attr_cl[0].val.clusterDim.z = 1;
   cfg.attrs = attr_cl;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_line_fast<kAxial>, P, A);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_line_fast<kAxial, kU2, kLean>, P, A);
+  if (e != cudaSuccess) report_launch_error(e);
   ++g_launches;
+}
+
+template <bool kAxial>
+void launch_line(const DevProblem& P, const LineArgs& A, int nmax, cudaStream_t s) {
+  if (P.lean) {
+    if (!kAxial && P.source_kind == PCGPU_SOURCE_JOULE)
+      launch_line_t<kAxial, true, 2>(P, A, nmax, s);
+    else
+      launch_line_t<kAxial, true, 1>(P, A, nmax, s);
+  } else if (P.all_u2) {
+    launch_line_t<kAxial, true, 0>(P, A, nmax, s);
+  } else {
+    launch_line_t<kAxial, false, 0>(P, A, nmax, s);
+  }
 }
 
 }  // namespace

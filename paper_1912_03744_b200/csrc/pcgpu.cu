@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -149,6 +150,7 @@ enum Buf {
   kField,       // pcgpu_run: resident field (N)
   kPowN,        // bound power field (N)
   kPowT,        // bound power field (T)
+  kStage,       // host-API staging field (N), allocated on first use
   kNumBufs
 };
 
@@ -486,7 +488,7 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
     std::vector<int> layer(d->layer, d->layer + nr);
 
     // Tables, flattened.
-    std::vector<double> knots, vals, slopes;
+    std::vector<double> knots, vals, slopes, ivl;
     DevProblem& P = h->P;
     P.n_layers = d->n_layers;
     for (int m = 0; m < d->n_layers; ++m) {
@@ -502,20 +504,101 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
         for (int k = 0; k < t.n; ++k) {
           knots.push_back(t.t[k]);
           vals.push_back(t.v[k]);
-          slopes.push_back(k == 0 ? 0.0 : (t.v[k] - t.v[k - 1]) / (t.t[k] - t.t[k - 1]));
+          const double sl = k == 0 ? 0.0 : (t.v[k] - t.v[k - 1]) / (t.t[k] - t.t[k - 1]);
+          slopes.push_back(sl);
+          // packed interval k: {t[k-1], t[k], v[k-1], slope_k}
+          ivl.push_back(k == 0 ? t.t[0] : t.t[k - 1]);
+          ivl.push_back(t.t[k]);
+          ivl.push_back(k == 0 ? t.v[0] : t.v[k - 1]);
+          ivl.push_back(sl);
         }
-        if (t.n >= 3) {
+        if (t.n > 0) {
+          P.mats[m].t_first[p] = t.t[0];
+          P.mats[m].t_last[p] = t.t[t.n - 1];
+          P.mats[m].v_first[p] = t.v[0];
+          P.mats[m].v_last[p] = t.v[t.n - 1];
+        }
+        if (t.n == 2) {
+          // a single interval: the bracket is always k = 1
+          P.mats[m].uniform[p] = 2;
+          P.mats[m].inv_h[p] = 0.0;
+        } else if (t.n >= 3) {
           // Uniform-knot bracket guess (exactness is kept by the device fix-up).
           const double inv_h = (t.n - 1) / (t.t[t.n - 1] - t.t[0]);
           double worst = 0;
           for (int k = 0; k < t.n; ++k)
             worst = std::max(worst, std::fabs((t.t[k] - t.t[0]) * inv_h - k));
-          if (worst < 0.25) {
+          if (worst < 0.5) {
             P.mats[m].uniform[p] = 1;
             P.mats[m].inv_h[p] = inv_h;
+            // Exactly uniform with a power-of-two step: the bracket is exact.
+            const double h = t.t[1] - t.t[0];
+            int ex;
+            const bool pow2 = h > 0 && std::frexp(h, &ex) == 0.5;
+            bool exact = pow2 && std::isfinite(t.t[0]);
+            for (int k = 0; exact && k < t.n; ++k)
+              exact = t.t[k] == t.t[0] + k * h && (t.t[k] - t.t[0]) * (1.0 / h) == k;
+            if (exact) {
+              P.mats[m].uniform[p] = 2;
+              P.mats[m].inv_h[p] = 1.0 / h;
+            }
           }
         }
       }
+    }
+    P.all_u2 = 1;
+    for (int m = 0; m < d->n_layers; ++m)
+      for (int p = 0; p < 3; ++p)
+        if (P.mats[m].n[p] > 0 && P.mats[m].uniform[p] != 2) P.all_u2 = 0;
+    // Lean fast kernels: MeanTemperature faces, Clamp policy, Joule/Null
+    // source, every table exactly uniform and one knot grid per property.
+    P.lean = P.all_u2 && d->halfpoint_rule == PCGPU_HALFPOINT_MEAN_TEMPERATURE &&
+             d->range_policy == PCGPU_RANGE_CLAMP && d->source_kind != PCGPU_SOURCE_FIELD;
+    for (int p = 0; p < 3 && P.lean; ++p) {
+      int ref = -1;
+      for (int m = 0; m < d->n_layers; ++m) {
+        if (P.mats[m].n[p] == 0) {
+          if (p < 2) P.lean = 0;  // cv / lambda are mandatory
+          continue;
+        }
+        if (ref < 0) { ref = m; continue; }
+        const DevMaterial &a = P.mats[ref], &b = P.mats[m];
+        if (a.n[p] != b.n[p] || a.t_first[p] != b.t_first[p] || a.t_last[p] != b.t_last[p] ||
+            a.inv_h[p] != b.inv_h[p])
+          P.lean = 0;
+      }
+    }
+    if (d->source_kind == PCGPU_SOURCE_JOULE && P.mats[d->source_layer].n[2] == 0) P.lean = 0;
+    if (std::getenv("PCGPU_NO_LEAN")) P.lean = 0;
+    std::vector<double> lt;  // lean table, uploaded below
+    if (P.lean) {
+      // property-grouped lean table: (prop, layer, k) -> {v[k-1], slope_k}
+      for (int p = 0; p < 3; ++p) {
+        int ref = -1;
+        for (int m = 0; m < d->n_layers; ++m)
+          if (P.mats[m].n[p] > 0) { ref = m; break; }
+        const int n = ref >= 0 ? P.mats[ref].n[p] : 1;
+        P.lean_base[p] = static_cast<int>(lt.size() / 2);
+        P.lean_stride[p] = n;
+        P.lean_kmax[p] = n - 1 < 1 ? 1 : n - 1;
+        P.lean_t0[p] = ref >= 0 ? P.mats[ref].t_first[p] : 0.0;
+        P.lean_tK[p] = ref >= 0 ? P.mats[ref].t_last[p] : 0.0;
+        P.lean_inv_h[p] = ref >= 0 ? P.mats[ref].inv_h[p] : 0.0;
+        P.lean_h[p] = P.lean_inv_h[p] > 0.0 ? 1.0 / P.lean_inv_h[p] : 0.0;
+        for (int m = 0; m < d->n_layers; ++m) {
+          for (int k = 0; k < n; ++k) {
+            if (P.mats[m].n[p] == n && k >= 1) {
+              const int o = P.mats[m].off[p] + k;
+              lt.push_back(vals[o - 1]);
+              lt.push_back(slopes[o]);
+            } else {
+              lt.push_back(0.0);
+              lt.push_back(0.0);
+            }
+          }
+        }
+      }
+      for (int m = 0; m < d->n_layers; ++m) P.lean_rho[m] = d->materials[m].rho;
     }
     P.nr = nr;
     P.nz = nz;
@@ -530,6 +613,9 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
     h->dev_allocs.push_back(dlayer);
     P.layer = dlayer;
     P.face_r_lo = up(face_r_lo);
+    std::vector<double> gfac(nr + 1, 0.0);
+    for (int i = 0; i < nr; ++i) gfac[i] = face_r_lo[i] * inv_gap_r[i];
+    P.gfac_r = up(gfac);
     P.inv_gap_r = up(inv_gap_r);
     P.inv_vol_r = up(inv_vol_r);
     P.gap_z = up(gap_z);
@@ -540,6 +626,8 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
     P.knots = up(knots);
     P.vals = up(vals);
     P.slopes = up(slopes);
+    if (P.lean) P.lean_tab = up(lt);
+    P.ivl = up(ivl);
     P.source_kind = d->source_kind;
     P.source_layer = d->source_layer;
     P.amplitude = d->amplitude;
@@ -565,6 +653,7 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
     for (int b = 0; b < kNumBufs; ++b) {
       if ((b == kPowN || b == kPowT) && d->source_kind != PCGPU_SOURCE_FIELD) continue;
       if ((b == kW || b == kKbar) && d->mode == PCGPU_MODE_FAST) continue;  // exact-mode only
+      if (b == kStage) continue;  // lazily, by the *_host entry points
       double* p = nullptr;
       CK(cudaMalloc(&p, bytes));
       h->dev_allocs.push_back(p);
@@ -721,10 +810,20 @@ int pcgpu_run(pcgpu_stepper* h, double* field, double t0, int32_t nsteps,
   return rc;
 }
 
+static void ensure_stage(pcgpu_stepper* h) {
+  if (h->buf[kStage]) return;
+  double* p = nullptr;
+  CK(cudaMalloc(&p, sizeof(double) * h->cells()));
+  h->dev_allocs.push_back(p);
+  CK(cudaMemsetAsync(p, 0, sizeof(double) * h->cells(), h->stream));
+  h->buf[kStage] = p;
+}
+
 int pcgpu_step_host(pcgpu_stepper* h, double* field_host, double t, pcgpu_step_result* r) {
   if (!h || !field_host) return PCGPU_ERR_ARG;
   GUARD_BEGIN
-  double* f = h->buf[kField];
+  ensure_stage(h);
+  double* f = h->buf[kStage];
   CK(cudaMemcpyAsync(f, field_host, sizeof(double) * h->cells(), cudaMemcpyHostToDevice,
                      h->stream));
   const int rc = pcgpu_step(h, f, t, r);
@@ -739,8 +838,9 @@ int pcgpu_step_host(pcgpu_stepper* h, double* field_host, double t, pcgpu_step_r
 static int half_host(pcgpu_stepper* h, bool radial, const double* in_host, double t, double tau,
                      double* out_host, pcgpu_outcome* o) {
   GUARD_BEGIN
+  ensure_stage(h);
   double* in = h->buf[kField];
-  double* out = h->buf[kNext];
+  double* out = h->buf[kStage];
   CK(cudaMemcpyAsync(in, in_host, sizeof(double) * h->cells(), cudaMemcpyHostToDevice,
                      h->stream));
   CK(cudaMemcpyAsync(out, out_host, sizeof(double) * h->cells(), cudaMemcpyHostToDevice,
