@@ -129,7 +129,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default=os.environ.get("PCGPU_BENCH_MODE", "exact"),
+    ap.add_argument("--mode", default=os.environ.get("PCGPU_BENCH_MODE", "fast"),
                     choices=["exact", "fast"])
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--cpu-nz", type=int, default=512, help="z-slice of the CPU sample")
@@ -221,7 +221,10 @@ def main():
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(f"{args.mode}:{dom}")
+            tr = json.load(f).get(f"{args.config}:{args.mode}:{dom}")
+        if tr:
+            traffic = tr["dram_bytes_per_launch"] / 1e9
+            traffic_src = tr.get("source")
 
     # e2e through the reference-facing C-ABI with HOST buffers: pcgpu_step_host
     # copies the field H2D, steps, copies D2H every step.
@@ -270,6 +273,7 @@ def main():
                                    "halvings": stats["halvings"], "steps": stats["steps"]}),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "traffic_unit": "GB per launch (ncu dram__bytes_read+write)",
                          "kernel": f"{dom} Picard iteration ({args.mode})",
                          "bytes_per_launch": per_launch_bytes, "launches": dom_n,
                          "ms_per_launch": dom_ms / max(dom_n, 1), "peak_kind": peak_kind,

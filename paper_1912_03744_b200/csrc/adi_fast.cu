@@ -31,7 +31,9 @@
 #include <cooperative_groups.h>
 
 #include <cstdint>
+#include <cstddef>
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "adi_kernels.h"
@@ -165,8 +167,8 @@ struct LineArgs {
 // source term in the sweep; 2 = lean with the Joule source (radial sweep).
 // Lean requires: MeanTemperature faces, Clamp policy, every table exactly
 // uniform (power-of-two step) with one knot grid per property across layers.
-template <bool kAxial, bool kU2, int kLean>
-__global__ void __launch_bounds__(NT, 3) k_line_fast(DevProblem P, LineArgs A) {
+template <bool kAxial, bool kU2, int kLean, bool kDirect = false>
+__global__ void __launch_bounds__(NT, kDirect ? 4 : 3) k_line_fast(DevProblem P, LineArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FastSmem& S = *reinterpret_cast<FastSmem*>(smem_raw);
   if (skip_iteration(A.st, A.it, A.eps)) return;
@@ -185,7 +187,9 @@ __global__ void __launch_bounds__(NT, 3) k_line_fast(DevProblem P, LineArgs A) {
 
   // ---- stage the segment's rows (coalesced cp.async, zero-filled past n) ----
   const int nseg = max(0, min(SEG, n - seg0));
-  if ((A.ld & 1) == 0) {
+  if (kDirect) {
+    // rows are read straight into registers below (no shared-memory tiles)
+  } else if ((A.ld & 1) == 0) {
     for (int e = 2 * tid; e < SEG; e += 2 * NT) {
       const int valid = max(0, min(2, nseg - e));
       const int r = seg0 + (valid ? e : 0);
@@ -204,7 +208,7 @@ __global__ void __launch_bounds__(NT, 3) k_line_fast(DevProblem P, LineArgs A) {
       cp_async8(smem_u32(S.ex.v) + o, gEx + r, valid * 8);
     }
   }
-  if (tid == 0) {
+  if (!kDirect && tid == 0) {
     const bool lo = seg0 >= 1 && seg0 - 1 < n;
     const bool hi = seg0 + SEG < n;
     S.halo[0] = lo ? gTs[seg0 - 1] : 0.0;
@@ -233,16 +237,54 @@ __global__ void __launch_bounds__(NT, 3) k_line_fast(DevProblem P, LineArgs A) {
   // Row index k in [-1, R] of the chunk <-> global row s + k.
   const int s = seg0 + tid * R;
   const int e0 = tid * R;
+  // Direct variant: the chunk's rows (and one halo row each side) are loaded
+  // with 16-B vector loads straight into registers; no shared-memory tiles.
+  double rts[R + 2], rta[R + 2], rex[R];
+  if (kDirect) {
+    const bool full = s + R <= n;
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < R / 2; ++q) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(gTs + s) + q);
+        const double2 b = __ldg(reinterpret_cast<const double2*>(gTa + s) + q);
+        const double2 c = __ldg(reinterpret_cast<const double2*>(gEx + s) + q);
+        rts[2 * q + 1] = a.x; rts[2 * q + 2] = a.y;
+        rta[2 * q + 1] = b.x; rta[2 * q + 2] = b.y;
+        rex[2 * q] = c.x; rex[2 * q + 1] = c.y;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const bool v = s + k < n;
+        const int r = v ? s + k : 0;
+        rts[k + 1] = v ? __ldg(gTs + r) : 0.0;
+        rta[k + 1] = v ? __ldg(gTa + r) : 0.0;
+        rex[k] = v ? __ldg(gEx + r) : 0.0;
+      }
+    }
+    const bool lo = s >= 1 && s - 1 < n;
+    const bool hi = s + R < n;
+    rts[0] = lo ? __ldg(gTs + s - 1) : 0.0;
+    rta[0] = lo ? __ldg(gTa + s - 1) : 0.0;
+    rts[R + 1] = hi ? __ldg(gTs + s + R) : 0.0;
+    rta[R + 1] = hi ? __ldg(gTa + s + R) : 0.0;
+  }
   auto ld_ts = [&](int k) -> double {
+    if (kDirect) return rts[k + 1];
     if (k < 0) return tid > 0 ? tile_get(S.ts, e0 - 1) : S.halo[0];
     if (k >= R) return tid < NT - 1 ? tile_get(S.ts, e0 + R) : S.halo[2];
     return tile_get(S.ts, e0 + k);
   };
   auto ld_ta = [&](int k) -> double {
+    if (kDirect) return rta[k + 1];
     if (k < 0) return tid > 0 ? tile_get(S.ta, e0 - 1) : S.halo[1];
     if (k >= R) return tid < NT - 1 ? tile_get(S.ta, e0 + R) : S.halo[3];
     return tile_get(S.ta, e0 + k);
   };
+  auto ld_ex = [&](int k) -> double { return kDirect ? rex[k] : tile_get(S.ex, e0 + k); };
+  // final update: re-read (L1/L2-resident) so the row registers die after assembly
+  auto fin_ts = [&](int k) -> double { return kDirect ? __ldg(gTs + min(s + k, n - 1)) : ld_ts(k); };
+  auto fin_ta = [&](int k) -> double { return kDirect ? __ldg(gTa + min(s + k, n - 1)) : ld_ta(k); };
   // Face f = s + k (between rows f-1 and f): conductance and anchor flux.
   auto face = [&](int k, double ts_lo, double ts_hi, double ta_lo, double ta_hi, double& c,
                   double& flux) {
@@ -319,7 +361,7 @@ __global__ void __launch_bounds__(NT, 3) k_line_fast(DevProblem P, LineArgs A) {
       }
       const double fc_hi = vf ? c : 0.0;
       const double fl_hi = fc_hi * (ta_n - ta_c);
-      const double exk = tile_get(S.ex, e0 + k);
+      const double exk = ld_ex(k);
       double Ak, Ck, bk, dk;
       if (kAxial) {
         const double inv_eta = __ldg(P.inv_eta + min(i, P.nz - 1));
@@ -392,7 +434,7 @@ __global__ void __launch_bounds__(NT, 3) k_line_fast(DevProblem P, LineArgs A) {
       const int i = s + k;
       double Ak = 0.0, Ck = 0.0, bk = 1.0, dk = 0.0;
       if (i < n) {
-        const double exk = tile_get(S.ex, e0 + k);
+        const double exk = ld_ex(k);
         if (kAxial) {
           const double inv_eta = P.inv_eta[i];
           Ak = fc_lo * inv_eta;
@@ -568,7 +610,42 @@ __global__ void __launch_bounds__(NT, 3) k_line_fast(DevProblem P, LineArgs A) {
 
   // ---- back substitution, update, delta, staged store ----
   double dmax = 0.0;
-  {
+  double* gOut = A.out + lbase;
+  if (kDirect) {
+    double ro[R];
+    double xn = Q;
+    ro[R - 1] = xn;
+    double x = up[R - 2] + Qprev * vp[R - 2] + wp * Q;
+#pragma unroll
+    for (int k = R - 2; k >= 0; --k) {
+      if (k < R - 2) x = up[k] + Qprev * vp[k] - cp[k] * xn;
+      ro[k] = x;
+      xn = x;
+    }
+    const bool full = s + R <= n;
+#pragma unroll
+    for (int q = 0; q < R / 2; ++q) {
+      double o0 = 0.0, o1 = 0.0;
+      if (full) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(gTa + s) + q);
+        const double2 t = __ldg(reinterpret_cast<const double2*>(gTs + s) + q);
+        o0 = a.x + ro[2 * q];
+        o1 = a.y + ro[2 * q + 1];
+        dmax = ref_max(dmax, fabs(o0 - t.x));
+        dmax = ref_max(dmax, fabs(o1 - t.y));
+        reinterpret_cast<double2*>(gOut + s)[q] = make_double2(o0, o1);
+      } else {
+        for (int h = 0; h < 2; ++h) {
+          const int k = 2 * q + h;
+          if (s + k < n) {
+            const double o = fin_ta(k) + ro[k];
+            dmax = ref_max(dmax, fabs(o - fin_ts(k)));
+            gOut[s + k] = o;
+          }
+        }
+      }
+    }
+  } else {
     double xn = Q;
     const int kl = R - 1;
     if (s + kl < n) {
@@ -589,8 +666,9 @@ __global__ void __launch_bounds__(NT, 3) k_line_fast(DevProblem P, LineArgs A) {
     }
   }
   __syncthreads();
-  double* gOut = A.out + lbase;
-  if ((A.ld & 1) == 0) {
+  if (kDirect) {
+    // stored directly above
+  } else if ((A.ld & 1) == 0) {
     for (int e = 2 * tid; e < nseg; e += 2 * NT) {
       const double2 v = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(S.ex.v) + swz(e));
       if (e + 1 < nseg) {
@@ -717,13 +795,14 @@ void report_launch_error(cudaError_t e) {
   fprintf(stderr, "pcgpu: k_line_fast launch failed: %s\n", cudaGetErrorString(e));
 }
 
-template <bool kAxial, bool kU2, int kLean>
+template <bool kAxial, bool kU2, int kLean, bool kDirect = false>
 void launch_line_t(const DevProblem& P, const LineArgs& A, int nmax, cudaStream_t s) {
   const int CL = (nmax + SEG - 1) / SEG;
-  const size_t smem = sizeof(FastSmem);
+  // the direct variant never touches the staging tiles (the struct's tail)
+  const size_t smem = kDirect ? offsetof(FastSmem, ts) : sizeof(FastSmem);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_line_fast<kAxial, kU2, kLean>,
+    cudaFuncSetAttribute(k_line_fast<kAxial, kU2, kLean, kDirect>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
@@ -739,14 +818,22 @@ void launch_line_t(const DevProblem& P, const LineArgs& A, int nmax, cudaStream_
   attr_cl[0].val.clusterDim.z = 1;
   cfg.attrs = attr_cl;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_line_fast<kAxial, kU2, kLean>, P, A);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_line_fast<kAxial, kU2, kLean, kDirect>, P, A);
   if (e != cudaSuccess) report_launch_error(e);
   ++g_launches;
 }
 
 template <bool kAxial>
 void launch_line(const DevProblem& P, const LineArgs& A, int nmax, cudaStream_t s) {
-  if (P.lean) {
+  // Direct (register) row loads measured slower than the swizzled cp.async
+  // tiles on B200 (4.3 vs 3.5 ms per cfg3 radial launch): opt-in only.
+  static const bool direct = std::getenv("PCGPU_DIRECT") != nullptr;
+  if (P.lean && direct && (A.ld & 1) == 0) {
+    if (!kAxial && P.source_kind == PCGPU_SOURCE_JOULE)
+      launch_line_t<kAxial, true, 2, true>(P, A, nmax, s);
+    else
+      launch_line_t<kAxial, true, 1, true>(P, A, nmax, s);
+  } else if (P.lean) {
     if (!kAxial && P.source_kind == PCGPU_SOURCE_JOULE)
       launch_line_t<kAxial, true, 2>(P, A, nmax, s);
     else
