@@ -126,7 +126,7 @@ def run_reference_cpu(case, steps: int, warmup: int, nz_sample: int, workers: in
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default=os.environ.get("PCGPU_BENCH_MODE", "fast"),
@@ -175,6 +175,10 @@ def main():
     g = case.grid()
     nr, nz = g.nr(), g.nz()
     active = g.active_cells()
+    if world > 1:
+        run_partitioned(args, case, rank, world, local, pg, grid_desc, metric)
+        pg.destroy_process_group()
+        return
     stepper = gpu_stepper_for(case, args.mode, local)
     field = torch.full((nz, nr), case.solver.T0, dtype=torch.float64, device=f"cuda:{local}").t()
     t = 0.0
@@ -284,6 +288,67 @@ def main():
         print(json.dumps(line))
     if pg:
         pg.destroy_process_group()
+
+
+def run_partitioned(args, case, rank, world, local, pg, grid_desc, metric):
+    """configs[3] partitioned over `world` GPUs: z-slabs for the radial sweep,
+    NCCL all-to-all transpose to r-slabs for the axial sweep, NCCL allreduce
+    of the Picard norm. Total work is fixed: strong scaling."""
+    import torch
+    from paper_1912_03744_b200.configs import make_source
+    from paper_1912_03744_b200.dist import PartitionedAdi, share_unique_id
+    g = case.grid()
+    dev = torch.device(f"cuda:{local}")
+    uid = share_unique_id(rank, dev)
+    part = PartitionedAdi(g, case.materials, make_source(case, g), case.timing, case.solver,
+                          device=local, rank=rank, world=world, unique_id=uid)
+    field = torch.full((g.nz(), g.nr()), case.solver.T0, dtype=torch.float64, device=dev).t()
+    part.set_field(field)
+    t, _, _ = part.run(0.0, args.warmup)
+    stream = torch.cuda.ExternalStream(part.stream(), device=dev)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    l0 = part.launch_count()
+    pg.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        t_end, stats, _ = part.run(t, args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    pg.barrier()
+    ms_t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+    pg.all_reduce(ms_t, op=pg.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    launches = part.launch_count() - l0
+    # transpose time, measured separately (synchronising events per transpose)
+    part.enable_timing(True)
+    part.run(t_end, 1)
+    tm = part.timing()
+    tr = torch.tensor([tm["transpose_ms"] / max(tm["transposes"], 1)], dtype=torch.float64,
+                      device=dev)
+    pg.all_reduce(tr, op=pg.ReduceOp.MAX)
+    # every rank counts the whole grid's cell-updates (the norm is global)
+    value = stats["cell_updates"] / (ms_max / 1e3)
+    if rank == 0:
+        z0, z1, r0, r1 = part.slabs()
+        line = {
+            "metric": metric, "value": value, "unit": "cell-updates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": dict(grid_desc, mode="fast", parallelism=f"z-slab/r-slab x{world}",
+                           l2="inputs > L2", rank0_slabs={"z": [z0, z1], "r": [r0, r1]},
+                           picard={"radial_iters": stats["radial_iterations"],
+                                   "axial_iters": stats["axial_iterations"],
+                                   "halvings": stats["halvings"]}),
+            "transpose": {"ms_per_transpose_max_rank": float(tr.item()),
+                          "transposes_per_step": 2, "fields_per_transpose": 2,
+                          "bytes_per_rank_per_transpose":
+                              2 * 8 * g.nr() * g.nz() // world * (world - 1) // world},
+            "clocks": clk.summary(), "gpu_launches": launches, "e2e": None,
+        }
+        print(json.dumps(line))
 
 
 def gpu_stepper_for(case, mode, device):

@@ -221,6 +221,43 @@ int pcgpu_enable_kernel_timing(pcgpu_stepper* h, int32_t on);
 /* Number of this library's kernels launched since creation. */
 int64_t pcgpu_launch_count(const pcgpu_stepper* h);
 
+/* ---- Partitioned stepper: one node of B200s ------------------
+ * z-slabs (radial lines j) for the radial sweep, r-slabs (axial lines i) for
+ * the axial sweep, all-to-all transposes between them, allreduce(max) of the
+ * Picard norm every iteration. Fast-mode kernels; bit-identical to a
+ * single-GPU fast-mode run. With nccl_id == NULL the library emulates
+ * `nranks` ranks in this process on desc->device (test/validation mode);
+ * otherwise this process is rank `rank` of an NCCL communicator created from
+ * the 128-byte id produced by pcgpu_nccl_unique_id on one rank and shared by
+ * the caller (e.g. torch.distributed broadcast). No reference equivalent: the
+ * reference is shared-memory only. */
+typedef struct pcgpu_dist pcgpu_dist;
+int pcgpu_nccl_unique_id(void* id128);
+int pcgpu_dist_create(const pcgpu_desc* desc, int32_t rank, int32_t nranks, const void* nccl_id,
+                      pcgpu_dist** out);
+void pcgpu_dist_destroy(pcgpu_dist* h);
+const char* pcgpu_dist_last_error(const pcgpu_dist* h);
+/* Slab boundaries for nranks ranks (host only): zb/rb have nranks+1 entries;
+ * rank p owns radial lines j in [zb[p], zb[p+1]) and axial lines i in
+ * [rb[p], rb[p+1]). Balanced by active cells. */
+int pcgpu_dist_plan(const pcgpu_desc* desc, int32_t nranks, int32_t* zb, int32_t* rb);
+int pcgpu_dist_slabs(const pcgpu_dist* h, int32_t* z0, int32_t* z1, int32_t* r0, int32_t* r1);
+/* Every rank passes the full initial field (device, nr x nz column-major). */
+int pcgpu_dist_set_field(pcgpu_dist* h, const double* field_dev);
+/* Writes this process's z-slab lines into the full-size device field. */
+int pcgpu_dist_get_field(pcgpu_dist* h, double* field_dev);
+/* nsteps x step() with t += tau_used on the partitioned state. */
+int pcgpu_dist_run(pcgpu_dist* h, double t0, int32_t nsteps, pcgpu_step_result* results,
+                   pcgpu_run_stats* stats);
+void* pcgpu_dist_stream(const pcgpu_dist* h);
+/* Kernels launched by this library in this process so far. */
+int64_t pcgpu_dist_launch_count(const pcgpu_dist* h);
+int pcgpu_dist_enable_timing(pcgpu_dist* h, int32_t on);
+/* Accumulated all-to-all transpose time (pack + exchange + unpack), counts,
+ * and Picard line-kernel time, since timing was enabled. */
+int pcgpu_dist_timing(const pcgpu_dist* h, double* transpose_ms, int64_t* transposes,
+                      int64_t* allreduces, double* radial_ms, double* axial_ms);
+
 /* ---- Batched tridiagonal systems (BASELINE configs[1]) ----------
  * thomas_solve_inplace (tridiagonal.hpp:25-42) applied to `batch` independent
  * systems of size n, all device pointers. Layouts:

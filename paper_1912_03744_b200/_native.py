@@ -76,7 +76,10 @@ EXPORTS = [
     "pcgpu_axial_half_step", "pcgpu_step", "pcgpu_step_host", "pcgpu_radial_half_step_host",
     "pcgpu_axial_half_step_host", "pcgpu_run", "pcgpu_clamp_events", "pcgpu_stream",
     "pcgpu_kernel_timing", "pcgpu_enable_kernel_timing", "pcgpu_launch_count",
-    "pcgpu_tridiag_batch",
+    "pcgpu_tridiag_batch", "pcgpu_nccl_unique_id", "pcgpu_dist_create", "pcgpu_dist_destroy",
+    "pcgpu_dist_last_error", "pcgpu_dist_plan", "pcgpu_dist_slabs", "pcgpu_dist_set_field",
+    "pcgpu_dist_get_field", "pcgpu_dist_run", "pcgpu_dist_stream", "pcgpu_dist_enable_timing",
+    "pcgpu_dist_timing", "pcgpu_dist_launch_count",
 ]
 
 _lib = None
@@ -124,6 +127,24 @@ def load():
         "pcgpu_launch_count": (C.c_int64, [vp]),
         "pcgpu_tridiag_batch": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, C.c_int64, C.c_int32,
                                           C.c_int32, vp, C.POINTER(C.c_int64)]),
+        "pcgpu_nccl_unique_id": (C.c_int, [vp]),
+        "pcgpu_dist_create": (C.c_int, [C.POINTER(Desc), C.c_int32, C.c_int32, vp,
+                                        C.POINTER(vp)]),
+        "pcgpu_dist_destroy": (None, [vp]),
+        "pcgpu_dist_last_error": (C.c_char_p, [vp]),
+        "pcgpu_dist_plan": (C.c_int, [C.POINTER(Desc), C.c_int32, C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_int32)]),
+        "pcgpu_dist_slabs": (C.c_int, [vp] + [C.POINTER(C.c_int32)] * 4),
+        "pcgpu_dist_set_field": (C.c_int, [vp, vp]),
+        "pcgpu_dist_get_field": (C.c_int, [vp, vp]),
+        "pcgpu_dist_run": (C.c_int, [vp, C.c_double, C.c_int32, C.POINTER(StepResultC),
+                                     C.POINTER(RunStats)]),
+        "pcgpu_dist_stream": (vp, [vp]),
+        "pcgpu_dist_launch_count": (C.c_int64, [vp]),
+        "pcgpu_dist_enable_timing": (C.c_int, [vp, C.c_int32]),
+        "pcgpu_dist_timing": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                        C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                        C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -155,7 +155,8 @@ struct LineArgs {
   const double* pw;  // bound power field (N layout) for PCGPU_SOURCE_FIELD, or null
   double* out;
   long long ld;      // line stride in elements
-  int nlines;
+  int nlines;        // lines in this launch
+  int line0;         // global index of the first line (slab offset)
   int it;
   double eps, hk, pulse;
   DevStatus* st;
@@ -176,11 +177,12 @@ __global__ void __launch_bounds__(NT, kDirect ? 4 : 3) k_line_fast(DevProblem P,
   cg::cluster_group cluster = cg::this_cluster();
   const int CL = static_cast<int>(cluster.num_blocks());
   const int rank = static_cast<int>(cluster.block_rank());
-  const int line = blockIdx.x / CL;
+  const int lline = blockIdx.x / CL;    // line within this launch's slab
+  const int line = A.line0 + lline;     // global line index (masks, layers, errors)
   const int tid = threadIdx.x;
   const int n = kAxial ? col_extent(P, line) : row_extent(P, line);
   const int seg0 = rank * SEG;
-  const size_t lbase = static_cast<size_t>(line) * static_cast<size_t>(A.ld);
+  const size_t lbase = static_cast<size_t>(lline) * static_cast<size_t>(A.ld);
   const double* gTs = A.Ts + lbase;
   const double* gTa = A.Ta + lbase;
   const double* gEx = A.ex + lbase;
@@ -845,6 +847,116 @@ void launch_line(const DevProblem& P, const LineArgs& A, int nmax, cudaStream_t 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Slab variants for the partitioned (multi-GPU) stepper. A z-slab holds the
+// radial lines j in [j0, j0+nj) in N layout (line stride nr); an r-slab holds
+// the axial lines i in [i0, i0+ni) in T layout (line stride nz). The per-cell
+// arithmetic is exactly the single-GPU fast kernels', so a partitioned run is
+// bit-identical to a single-GPU fast run.
+
+// Lambda_r[T] + X(T) on a z-slab, N layout in and out (k_axial_rhs_fast
+// without the transpose).
+__global__ void __launch_bounds__(256)
+    k_rhs_zslab(DevProblem P, double pulse, int j0, int nj, const double* __restrict__ hN,
+                double* __restrict__ eN, DevStatus* st) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int jl = blockIdx.y * 8 + w;
+  if (jl >= nj) return;
+  const int j = j0 + jl;
+  const int n = row_extent(P, j);
+  const int i = blockIdx.x * 32 + lane;
+  const double* row = hN + static_cast<size_t>(jl) * P.nr;
+  const bool act = i < n;
+  const double ti = act ? row[i] : 0.0;
+  double fh = 0.0;
+  if (act && i < n - 1) {
+    const double tn = row[i + 1];
+    fh = P.face_r_lo[i + 1] * face_lambda_fast(P, P.layer[i], P.layer[i + 1], ti, tn, st, j) *
+         P.inv_gap_r[i + 1] * (tn - ti);
+  }
+  double flo = __shfl_up_sync(0xffffffffu, fh, 1);
+  if (lane == 0) {
+    flo = 0.0;
+    if (act && i > 0) {
+      const double tp = row[i - 1];
+      flo = P.face_r_lo[i] * face_lambda_fast<false>(P, P.layer[i - 1], P.layer[i], tp, ti, st, j) *
+            P.inv_gap_r[i] * (ti - tp);
+    }
+  }
+  if (act)
+    eN[static_cast<size_t>(jl) * P.nr + i] =
+        (fh - flo) * P.inv_vol_r[i] + source_power_fast(P, pulse, P.layer[i], ti, 0.0, st, j);
+}
+
+// Lambda_z[T] on an r-slab, T layout in and out (k_expl_axial_fast without the
+// transpose).
+__global__ void __launch_bounds__(256)
+    k_expl_rslab(DevProblem P, int i0, int ni, const double* __restrict__ fT,
+                 double* __restrict__ eT, DevStatus* st) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int il = blockIdx.y * 8 + w;
+  if (il >= ni) return;
+  const int i = i0 + il;
+  const int m = col_extent(P, i);
+  const int L = P.layer[i];
+  const int j = blockIdx.x * 32 + lane;
+  const double* row = fT + static_cast<size_t>(il) * P.nz;
+  const bool act = j < m;
+  const double tj = act ? row[j] : 0.0;
+  double fh = 0.0;
+  if (act) {
+    if (j < m - 1) {
+      const double tn = row[j + 1];
+      fh = face_lambda_fast(P, L, L, tj, tn, st, i) * P.inv_gap_z[j + 1] * (tn - tj);
+    } else if (L == 0 && !P.all_neumann) {
+      fh = mat_eval_fast(P, L, kLambda, P.T0, st, i) * (P.T0 - tj) * __drcp_rn(0.5 * P.width_z[j]);
+    }
+  }
+  double flo = __shfl_up_sync(0xffffffffu, fh, 1);
+  if (lane == 0) {
+    flo = 0.0;
+    if (act && j > 0) {
+      const double tp = row[j - 1];
+      flo = face_lambda_fast<false>(P, L, L, tp, tj, st, i) * P.inv_gap_z[j] * (tj - tp);
+    }
+  }
+  if (act) eT[static_cast<size_t>(il) * P.nz + j] = (fh - flo) * P.inv_eta[j];
+}
+
+}  // namespace
+
+void launch_radial_fast_slab(const DevProblem& P, int it, double eps, double half_k, double pulse,
+                             int j0, int nj, const double* TsN, const double* TcN,
+                             const double* explN, double* outN, DevStatus* st, cudaStream_t s) {
+  LineArgs A{TsN, TcN, explN, nullptr, outN, P.nr, nj, j0, it, eps, half_k, pulse, st};
+  if (nj > 0) launch_line<false>(P, A, P.nr, s);
+}
+
+void launch_axial_fast_slab(const DevProblem& P, int it, double eps, double half_k, int i0,
+                            int ni, const double* TsT, const double* ThT, const double* explT,
+                            double* outT, DevStatus* st, cudaStream_t s) {
+  LineArgs A{TsT, ThT, explT, nullptr, outT, P.nz, ni, i0, it, eps, half_k, 0.0, st};
+  if (ni > 0) launch_line<true>(P, A, P.nz, s);
+}
+
+void launch_rhs_zslab(const DevProblem& P, double pulse, int j0, int nj, const double* hN,
+                      double* eN, DevStatus* st, cudaStream_t s) {
+  if (nj <= 0) return;
+  dim3 grid((P.nr + 31) / 32, (nj + 7) / 8);
+  k_rhs_zslab<<<grid, 256, 0, s>>>(P, pulse, j0, nj, hN, eN, st);
+  ++g_launches;
+}
+
+void launch_expl_rslab(const DevProblem& P, int i0, int ni, const double* fT, double* eT,
+                       DevStatus* st, cudaStream_t s) {
+  if (ni <= 0) return;
+  dim3 grid((P.nz + 31) / 32, (ni + 7) / 8);
+  k_expl_rslab<<<grid, 256, 0, s>>>(P, i0, ni, fT, eT, st);
+  ++g_launches;
+}
+
+namespace {
 }  // namespace
 
 bool fast_supported(const DevProblem& P) {
@@ -854,14 +966,14 @@ bool fast_supported(const DevProblem& P) {
 void launch_radial_fast(const DevProblem& P, int it, double eps, double half_k, double pulse,
                         const double* TsN, const double* TcN, const double* explN,
                         const double* powN, double* outN, DevStatus* st, cudaStream_t s) {
-  LineArgs A{TsN, TcN, explN, powN, outN, P.nr, P.nz, it, eps, half_k, pulse, st};
+  LineArgs A{TsN, TcN, explN, powN, outN, P.nr, P.nz, 0, it, eps, half_k, pulse, st};
   launch_line<false>(P, A, P.nr, s);
 }
 
 void launch_axial_fast(const DevProblem& P, int it, double eps, double half_k, const double* TsT,
                        const double* ThT, const double* explT, double* outT, DevStatus* st,
                        cudaStream_t s) {
-  LineArgs A{TsT, ThT, explT, nullptr, outT, P.nz, P.nr, it, eps, half_k, 0.0, st};
+  LineArgs A{TsT, ThT, explT, nullptr, outT, P.nz, P.nr, 0, it, eps, half_k, 0.0, st};
   launch_line<true>(P, A, P.nz, s);
 }
 

@@ -56,6 +56,18 @@ void launch_axial_fast(const DevProblem& P, int it, double eps, double half_k, c
                        const double* ThT, const double* explT, double* outT, DevStatus* st,
                        cudaStream_t s);
 
+// ---- partitioned (multi-GPU) slabs, fast mode (adi_fast.cu) ----
+void launch_radial_fast_slab(const DevProblem& P, int it, double eps, double half_k, double pulse,
+                             int j0, int nj, const double* TsN, const double* TcN,
+                             const double* explN, double* outN, DevStatus* st, cudaStream_t s);
+void launch_axial_fast_slab(const DevProblem& P, int it, double eps, double half_k, int i0,
+                            int ni, const double* TsT, const double* ThT, const double* explT,
+                            double* outT, DevStatus* st, cudaStream_t s);
+void launch_rhs_zslab(const DevProblem& P, double pulse, int j0, int nj, const double* hN,
+                      double* eN, DevStatus* st, cudaStream_t s);
+void launch_expl_rslab(const DevProblem& P, int i0, int ni, const double* fT, double* eT,
+                       DevStatus* st, cudaStream_t s);
+
 // Kernel launch counter (for the bench's gpu_launches claim).
 extern unsigned long long g_launches;
 

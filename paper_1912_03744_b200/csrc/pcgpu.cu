@@ -430,41 +430,11 @@ struct pcgpu_stepper {
   }
 };
 
-#define GUARD_BEGIN try {
-#define GUARD_END(h)                                                                  \
-  }                                                                                   \
-  catch (const CudaError& ce) {                                                       \
-    return (h)->fail(PCGPU_ERR_CUDA, std::string(ce.what) + ": " + cudaGetErrorString(ce.e)); \
-  }
-
-extern "C" {
-
-int32_t pcgpu_abi_version(void) { return PCGPU_ABI_VERSION; }
-
-int pcgpu_device_count(int32_t* count) {
-  int n = 0;
-  if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
-  *count = n;
-  return PCGPU_OK;
-}
-
-int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
-  if (!d || !out) return PCGPU_ERR_ARG;
-  *out = nullptr;
-  const std::string v = validate(d);
-  if (!v.empty()) {
-    g_create_error = v;
-    return PCGPU_ERR_CONFIG;
-  }
-  auto h = std::make_unique<pcgpu_stepper>();
-  try {
-    h->d = *d;
-    CK(cudaSetDevice(d->device));
-    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-    const int nr = d->nr, nz = d->nz;
-    h->tau_floor = d->tau_min > 0 ? d->tau_min : 1e-12 * d->t_per;  // solver.hpp:28-30
-    for (int i = 0; i < nr; ++i) h->active += (i < d->nr_core ? nz : d->nz_shared);
-
+// DevProblem from the descriptor: metric reciprocals, flattened tables and
+// the fast-mode table forms, uploaded to the current device. Shared by the
+// single-GPU stepper and the partitioned (multi-GPU) stepper.
+void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& allocs) {
+  const int nr = d->nr, nz = d->nz;
     // Metric reciprocals exactly as the reference stepper computes them
     // (solver.cpp:146-159; geometry.hpp:87-94). Host code is compiled with
     // -ffp-contract=off, so these are the reference's bits.
@@ -489,7 +459,7 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
 
     // Tables, flattened.
     std::vector<double> knots, vals, slopes, ivl;
-    DevProblem& P = h->P;
+    
     P.n_layers = d->n_layers;
     for (int m = 0; m < d->n_layers; ++m) {
       const pcgpu_material& mt = d->materials[m];
@@ -606,11 +576,11 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
     P.nz_shared = d->nz_shared;
     auto up = [&](const std::vector<double>& v) {
       double* p = dev_upload(v);
-      h->dev_allocs.push_back(p);
+      allocs.push_back(p);
       return p;
     };
     int* dlayer = dev_upload(layer);
-    h->dev_allocs.push_back(dlayer);
+    allocs.push_back(dlayer);
     P.layer = dlayer;
     P.face_r_lo = up(face_r_lo);
     std::vector<double> gfac(nr + 1, 0.0);
@@ -638,8 +608,51 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
     unsigned long long* clamp = nullptr;
     CK(cudaMalloc(&clamp, sizeof(unsigned long long) * d->n_layers));
     CK(cudaMemset(clamp, 0, sizeof(unsigned long long) * d->n_layers));
-    h->dev_allocs.push_back(clamp);
+    allocs.push_back(clamp);
     P.clamp = clamp;
+}
+
+// Exported for pcgpu_dist.cu.
+std::string pcgpu_validate_desc(const pcgpu_desc* d) { return validate(d); }
+double pcgpu_host_initial_tau(const pcgpu_desc& d, double t) { return host_initial_tau(d, t); }
+double pcgpu_host_pulse_value(const pcgpu_desc& d, double t) { return host_pulse_value(d, t); }
+
+#define GUARD_BEGIN try {
+#define GUARD_END(h)                                                                  \
+  }                                                                                   \
+  catch (const CudaError& ce) {                                                       \
+    return (h)->fail(PCGPU_ERR_CUDA, std::string(ce.what) + ": " + cudaGetErrorString(ce.e)); \
+  }
+
+extern "C" {
+
+int32_t pcgpu_abi_version(void) { return PCGPU_ABI_VERSION; }
+
+int pcgpu_device_count(int32_t* count) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+  *count = n;
+  return PCGPU_OK;
+}
+
+int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
+  if (!d || !out) return PCGPU_ERR_ARG;
+  *out = nullptr;
+  const std::string v = validate(d);
+  if (!v.empty()) {
+    g_create_error = v;
+    return PCGPU_ERR_CONFIG;
+  }
+  auto h = std::make_unique<pcgpu_stepper>();
+  try {
+    h->d = *d;
+    CK(cudaSetDevice(d->device));
+    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    const int nr = d->nr, nz = d->nz;
+    h->tau_floor = d->tau_min > 0 ? d->tau_min : 1e-12 * d->t_per;  // solver.hpp:28-30
+    for (int i = 0; i < nr; ++i) h->active += (i < d->nr_core ? nz : d->nz_shared);
+
+    build_dev_problem(d, h->P, h->dev_allocs);
 
     CK(cudaMalloc(&h->st, sizeof(DevStatus)));
     h->dev_allocs.push_back(h->st);

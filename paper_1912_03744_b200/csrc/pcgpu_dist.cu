@@ -1,0 +1,697 @@
+// pcgpu_dist.cu -- partitioned ADI stepper for one node of B200s.
+//
+// The reference is shared-memory only (SPEC.md:389 lists distributed memory as
+// a non-goal); this is the B200-native scale-out of the same step:
+//
+//   z-slabs: rank p owns the radial lines j in Z_p (N layout, contiguous), so
+//            the radial Picard sweep is local;
+//   r-slabs: rank p owns the axial lines i in R_p (T layout, contiguous), so
+//            the axial Picard sweep is local;
+//   between the sweeps an all-to-all transpose moves the half-step field and
+//   its explicit term (Lambda_r[T_half] + X, computed on the z-slab where the
+//   radial stencil is local) from z-slabs to r-slabs; after an accepted step
+//   the new field and Lambda_z[T_new] (computed on the r-slab) move back;
+//   each Picard iteration's max-norm is an allreduce(max) of one uint64 (the
+//   bit pattern of a non-negative double), so every rank takes the same
+//   convergence / tau-halving decisions without host round trips.
+//
+// The per-cell and per-line arithmetic is exactly the single-GPU fast path's
+// (adi_fast.cu slab kernels), so a partitioned run is bit-identical to a
+// single-GPU fast run: tests run P "virtual ranks" in one process on one GPU
+// (Comm::Local) and compare bit-for-bit. Real ranks (one process per GPU)
+// use NCCL (grouped ncclSend/ncclRecv for the all-to-all, ncclAllReduce for
+// the norm), loaded with dlopen so the single-GPU library has no NCCL
+// dependency.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/pcgpu.h"
+#include "adi_kernels.h"
+
+using namespace pcgpu;
+
+// shared with pcgpu.cu
+void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& allocs);
+std::string pcgpu_validate_desc(const pcgpu_desc* d);
+double pcgpu_host_initial_tau(const pcgpu_desc& d, double t);
+double pcgpu_host_pulse_value(const pcgpu_desc& d, double t);
+
+namespace {
+
+struct DistError {
+  int code;
+  std::string what;
+};
+
+#define DCK(x)                                                                       \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess)                                                           \
+      throw DistError{PCGPU_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+// ---- NCCL via dlopen --------------------------------------------------------
+struct Nccl {
+  void* h = nullptr;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
+  decltype(&ncclGetErrorString) errorString = nullptr;
+
+  bool load(std::string& err) {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names)
+      if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) {
+      err = "pcgpu_dist: cannot dlopen libnccl.so.2";
+      return false;
+    }
+#define SYM(f, n) f = reinterpret_cast<decltype(f)>(dlsym(h, n))
+    SYM(getUniqueId, "ncclGetUniqueId");
+    SYM(commInitRank, "ncclCommInitRank");
+    SYM(commDestroy, "ncclCommDestroy");
+    SYM(allReduce, "ncclAllReduce");
+    SYM(send, "ncclSend");
+    SYM(recv, "ncclRecv");
+    SYM(groupStart, "ncclGroupStart");
+    SYM(groupEnd, "ncclGroupEnd");
+    SYM(errorString, "ncclGetErrorString");
+#undef SYM
+    if (!getUniqueId || !commInitRank || !allReduce || !send || !recv || !groupStart ||
+        !groupEnd) {
+      err = "pcgpu_dist: libnccl is missing symbols";
+      return false;
+    }
+    return true;
+  }
+} g_nccl;
+
+#define NCK(x)                                                                           \
+  do {                                                                                   \
+    ncclResult_t r_ = (x);                                                               \
+    if (r_ != ncclSuccess)                                                               \
+      throw DistError{PCGPU_ERR_CUDA, std::string(#x) + ": " +                           \
+                                          (g_nccl.errorString ? g_nccl.errorString(r_)   \
+                                                              : "nccl error")};          \
+  } while (0)
+
+// ---- small kernels ------------------------------------------------------------
+// dst[c * dst_ld + r] = src[r * src_ld + c] for r < rows, c < cols.
+__global__ void k_transpose_block(const double* __restrict__ src, long long src_ld, int rows,
+                                  int cols, double* __restrict__ dst, long long dst_ld) {
+  __shared__ double t[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
+  for (int rr = ly; rr < 32; rr += 8) {
+    const int r = r0 + rr, c = c0 + lx;
+    if (r < rows && c < cols) t[rr][lx] = src[static_cast<long long>(r) * src_ld + c];
+  }
+  __syncthreads();
+  for (int cc = ly; cc < 32; cc += 8) {
+    const int c = c0 + cc, r = r0 + lx;
+    if (r < rows && c < cols) dst[static_cast<long long>(c) * dst_ld + r] = t[lx][cc];
+  }
+}
+
+void transpose_block(const double* src, long long src_ld, int rows, int cols, double* dst,
+                     long long dst_ld, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return;
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32);
+  k_transpose_block<<<grid, 256, 0, s>>>(src, src_ld, rows, cols, dst, dst_ld);
+  ++g_launches;
+}
+
+// Local emulation of allreduce(max) of delta[it] and allreduce(min) of err
+// over P virtual ranks' status blocks.
+__global__ void k_reduce_status(DevStatus** st, int nranks, int it) {
+  if (threadIdx.x != 0) return;
+  unsigned long long dmax = 0, emin = kNoError;
+  for (int r = 0; r < nranks; ++r) {
+    dmax = max(dmax, st[r]->delta[it]);
+    emin = min(emin, st[r]->err);
+  }
+  for (int r = 0; r < nranks; ++r) {
+    st[r]->delta[it] = dmax;
+    st[r]->err = emin;
+  }
+}
+
+// Balanced contiguous split of n lines with per-line cell counts ext(l).
+template <typename F>
+std::vector<int> split_lines(int n, int parts, F ext) {
+  std::vector<double> pre(n + 1, 0.0);
+  for (int l = 0; l < n; ++l) pre[l + 1] = pre[l] + ext(l);
+  std::vector<int> b(parts + 1, 0);
+  b[parts] = n;
+  for (int p = 1; p < parts; ++p) {
+    const double target = pre[n] * p / parts;
+    int l = static_cast<int>(std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
+    b[p] = std::max(b[p - 1], std::min(l, n));
+  }
+  return b;
+}
+
+}  // namespace
+
+// One rank's slabs and buffers.
+struct RankState {
+  int rank = 0;
+  int j0 = 0, nj = 0;  // z-slab lines
+  int i0 = 0, ni = 0;  // r-slab lines
+  double *zTc = nullptr, *zExpl = nullptr, *zHalf = nullptr, *zIter = nullptr, *zR = nullptr;
+  double *rHalf = nullptr, *rExpl = nullptr, *rOut = nullptr, *rIter = nullptr;
+  double *send = nullptr, *recv = nullptr;
+  DevStatus* st = nullptr;
+};
+
+struct pcgpu_dist {
+  pcgpu_desc d{};
+  DevProblem P{};
+  std::vector<void*> allocs;
+  cudaStream_t stream = nullptr;
+  int nranks = 1;
+  bool local = true;  // P virtual ranks in this process
+  ncclComm_t comm = nullptr;
+  std::vector<int> zb, rb;  // slab boundaries (lines)
+  std::vector<RankState> ranks;  // local ranks (all of them in local mode)
+  DevStatus** st_dev_list = nullptr;
+  DevStatus* st_host = nullptr;
+  int64_t active = 0;
+  double tau_floor = 0;
+  std::string err;
+  int64_t err_line = -1;
+  int pred_r = 1, pred_a = 1;
+  // timing
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double transpose_ms = 0;
+  int64_t transposes = 0, allreduces = 0;
+  double radial_ms = 0, axial_ms = 0;
+  int64_t radial_launches = 0, axial_launches = 0;
+  bool timing = false;
+
+  ~pcgpu_dist() {
+    if (stream) cudaStreamSynchronize(stream);
+    if (comm && g_nccl.commDestroy) g_nccl.commDestroy(comm);
+    for (void* p : allocs) cudaFree(p);
+    if (st_host) cudaFreeHost(st_host);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  double* alloc(size_t n) {
+    double* p = nullptr;
+    DCK(cudaMalloc(&p, sizeof(double) * std::max<size_t>(n, 1)));
+    allocs.push_back(p);
+    return p;
+  }
+
+  int zcount(int p) const { return zb[p + 1] - zb[p]; }
+  int rcount(int p) const { return rb[p + 1] - rb[p]; }
+
+  // ---- collectives ----
+  void allreduce_status(int it) {
+    ++allreduces;
+    if (local) {
+      k_reduce_status<<<1, 32, 0, stream>>>(st_dev_list, nranks, it);
+      ++g_launches;
+      return;
+    }
+    RankState& R = ranks[0];
+    NCK(g_nccl.groupStart());
+    NCK(g_nccl.allReduce(&R.st->delta[it], &R.st->delta[it], 1, ncclUint64, ncclMax, comm,
+                         stream));
+    NCK(g_nccl.allReduce(&R.st->err, &R.st->err, 1, ncclUint64, ncclMin, comm, stream));
+    NCK(g_nccl.groupEnd());
+  }
+
+  // All-to-all transpose of two fields. z->r: sources are z-slab N-layout
+  // buffers (lines j, stride nr), destinations r-slab T-layout (lines i,
+  // stride nz). r->z the reverse. Packed block (p -> q) for z->r is
+  // [i in R_q][j in Z_p]; for r->z it is [j in Z_q][i in R_p].
+  void transpose(bool z2r, double* const* srcA, double* const* srcB, double* const* dstA,
+                 double* const* dstB) {
+    if (timing) DCK(cudaEventRecord(ev0, stream));
+    const int nr = d.nr, nz = d.nz;
+    // pack (every local rank, every destination)
+    for (size_t lr = 0; lr < ranks.size(); ++lr) {
+      RankState& R = ranks[lr];
+      size_t off = 0;
+      for (int q = 0; q < nranks; ++q) {
+        const int rows = z2r ? R.nj : R.ni;             // source lines owned
+        const int cols = z2r ? rcount(q) : zcount(q);   // destination's lines
+        const int c0 = z2r ? rb[q] : zb[q];
+        const long long ld = z2r ? nr : nz;
+        const size_t blk = static_cast<size_t>(rows) * cols;
+        transpose_block(srcA[lr] + c0, ld, rows, cols, R.send + off, rows, stream);
+        transpose_block(srcB[lr] + c0, ld, rows, cols, R.send + off + blk, rows, stream);
+        off += 2 * blk;
+      }
+    }
+    // exchange
+    if (local) {
+      for (int p = 0; p < nranks; ++p) {
+        size_t soff = 0;
+        for (int q = 0; q < nranks; ++q) {
+          const size_t blk = static_cast<size_t>(z2r ? zcount(p) * rcount(q)
+                                                     : rcount(p) * zcount(q));
+          // receiver q's staging: blocks ordered by source p
+          size_t roff = 0;
+          for (int pp = 0; pp < p; ++pp)
+            roff += 2 * static_cast<size_t>(z2r ? zcount(pp) * rcount(q) : rcount(pp) * zcount(q));
+          DCK(cudaMemcpyAsync(ranks[q].recv + roff, ranks[p].send + soff,
+                              sizeof(double) * 2 * blk, cudaMemcpyDeviceToDevice, stream));
+          soff += 2 * blk;
+        }
+      }
+    } else {
+      RankState& R = ranks[0];
+      const int me = R.rank;
+      NCK(g_nccl.groupStart());
+      size_t soff = 0, roff = 0;
+      for (int q = 0; q < nranks; ++q) {
+        const size_t sblk = static_cast<size_t>(z2r ? zcount(me) * rcount(q)
+                                                    : rcount(me) * zcount(q));
+        const size_t rblk = static_cast<size_t>(z2r ? zcount(q) * rcount(me)
+                                                    : rcount(q) * zcount(me));
+        if (sblk) NCK(g_nccl.send(R.send + soff, 2 * sblk, ncclDouble, q, comm, stream));
+        if (rblk) NCK(g_nccl.recv(R.recv + roff, 2 * rblk, ncclDouble, q, comm, stream));
+        soff += 2 * sblk;
+        roff += 2 * rblk;
+      }
+      NCK(g_nccl.groupEnd());
+    }
+    // unpack (2-D copies into the destination layout)
+    for (size_t lr = 0; lr < ranks.size(); ++lr) {
+      RankState& R = ranks[lr];
+      const int me = R.rank;
+      size_t off = 0;
+      for (int p = 0; p < nranks; ++p) {
+        // block from p: z2r -> [i in R_me][j in Z_p] into T layout lines i, cols j
+        //               r2z -> [j in Z_me][i in R_p] into N layout lines j, cols i
+        const int rows = z2r ? R.ni : R.nj;
+        const int cols = z2r ? zcount(p) : rcount(p);
+        const int c0 = z2r ? zb[p] : rb[p];
+        const size_t ld = z2r ? nz : nr;
+        const size_t blk = static_cast<size_t>(rows) * cols;
+        if (blk) {
+          DCK(cudaMemcpy2DAsync(dstA[lr] + c0, ld * sizeof(double), R.recv + off,
+                                cols * sizeof(double), cols * sizeof(double), rows,
+                                cudaMemcpyDeviceToDevice, stream));
+          DCK(cudaMemcpy2DAsync(dstB[lr] + c0, ld * sizeof(double), R.recv + off + blk,
+                                cols * sizeof(double), cols * sizeof(double), rows,
+                                cudaMemcpyDeviceToDevice, stream));
+        }
+        off += 2 * blk;
+        (void)me;
+      }
+    }
+    ++transposes;
+    if (timing) {
+      DCK(cudaEventRecord(ev1, stream));
+      DCK(cudaEventSynchronize(ev1));
+      float ms = 0;
+      DCK(cudaEventElapsedTime(&ms, ev0, ev1));
+      transpose_ms += ms;
+    }
+  }
+
+  void reset_status() {
+    for (RankState& R : ranks) {
+      DCK(cudaMemsetAsync(R.st->delta, 0, sizeof(R.st->delta), stream));
+      DCK(cudaMemsetAsync(&R.st->err, 0xff, sizeof(R.st->err), stream));
+    }
+  }
+
+  void fetch_status(int n) {
+    DevStatus* s0 = ranks[0].st;
+    DCK(cudaMemcpyAsync(st_host->delta, s0->delta, sizeof(unsigned long long) * (n + 1),
+                        cudaMemcpyDeviceToHost, stream));
+    DCK(cudaMemcpyAsync(&st_host->err, &s0->err, sizeof(s0->err), cudaMemcpyDeviceToHost,
+                        stream));
+    DCK(cudaStreamSynchronize(stream));
+  }
+
+  double delta_of(int it) const {
+    double v;
+    std::memcpy(&v, &st_host->delta[it], sizeof v);
+    return v;
+  }
+
+  // Picard loop over all local ranks with the norm allreduce after each
+  // iteration. Returns converged iteration, 0, or -error.
+  template <typename Launch>
+  int picard(int& pred, Launch&& launch, pcgpu_outcome* o, bool radial) {
+    const int max_iter = d.max_iter;
+    int launched = 0, batch = std::min(max_iter, std::max(1, pred) + 1);
+    *o = pcgpu_outcome{};
+    while (launched < max_iter) {
+      const int upto = std::min(max_iter, launched + batch);
+      for (int it = launched + 1; it <= upto; ++it) {
+        if (timing) DCK(cudaEventRecord(ev0, stream));
+        for (size_t lr = 0; lr < ranks.size(); ++lr) launch(lr, it);
+        if (timing) {
+          DCK(cudaEventRecord(ev1, stream));
+          DCK(cudaEventSynchronize(ev1));
+          float ms = 0;
+          DCK(cudaEventElapsedTime(&ms, ev0, ev1));
+          (radial ? radial_ms : axial_ms) += ms;
+          ++(radial ? radial_launches : axial_launches);
+        }
+        allreduce_status(it);
+      }
+      launched = upto;
+      fetch_status(launched);
+      if (st_host->err != kNoError) {
+        const int code = static_cast<int>(st_host->err & 7ull);
+        err_line = static_cast<int64_t>(st_host->err >> 3);
+        err = "line " + std::to_string(err_line) + " failed";
+        return -code;
+      }
+      for (int it = 1; it <= launched; ++it) {
+        const double dl = delta_of(it);
+        if (dl < d.epsilon) {
+          o->converged = 1;
+          o->iterations = it;
+          o->last_delta = dl;
+          pred = it;
+          return it;
+        }
+      }
+      batch = 2;
+    }
+    o->iterations = max_iter;
+    o->last_delta = delta_of(max_iter);
+    return 0;
+  }
+
+  // One ADI step (solver.cpp:356-373) on the partitioned state
+  // (z-slab anchor zTc + zExpl = Lambda_z[zTc]).
+  int step(double t, pcgpu_step_result* r, double* updates) {
+    double tau = pcgpu_host_initial_tau(d, t);
+    *r = pcgpu_step_result{};
+    for (;;) {
+      const double pulse = d.source_kind == PCGPU_SOURCE_JOULE
+                               ? pcgpu_host_pulse_value(d, t + 0.5 * tau) : 0.0;
+      const double hk = 2.0 / tau;
+      // ---- radial half-step on the z-slabs ----
+      reset_status();
+      auto zsrc = [&](RankState& R, int it) -> const double* {
+        return it == 1 ? R.zTc : (it % 2 == 0 ? R.zHalf : R.zIter);
+      };
+      auto zdst = [&](RankState& R, int it) -> double* { return it % 2 == 1 ? R.zHalf : R.zIter; };
+      int conv = picard(pred_r, [&](size_t lr, int it) {
+        RankState& R = ranks[lr];
+        launch_radial_fast_slab(P, it, d.epsilon, hk, pulse, R.j0, R.nj, zsrc(R, it), R.zTc,
+                                R.zExpl, zdst(R, it), R.st, stream);
+      }, &r->radial, true);
+      if (conv < 0) return -conv;
+      *updates += static_cast<double>(active) * r->radial.iterations;
+      if (conv > 0) {
+        // explicit radial term on the z-slab, then z -> r transpose of (T_half, expl)
+        std::vector<double*> hA(ranks.size()), hB(ranks.size()), dA(ranks.size()), dB(ranks.size());
+        for (size_t lr = 0; lr < ranks.size(); ++lr) {
+          RankState& R = ranks[lr];
+          hA[lr] = zdst(R, conv);
+          launch_rhs_zslab(P, pulse, R.j0, R.nj, hA[lr], R.zR, R.st, stream);
+          hB[lr] = R.zR;
+          dA[lr] = R.rHalf;
+          dB[lr] = R.rExpl;
+        }
+        transpose(true, hA.data(), hB.data(), dA.data(), dB.data());
+        // ---- axial half-step on the r-slabs ----
+        reset_status();
+        auto rsrc = [&](RankState& R, int it) -> const double* {
+          return it == 1 ? R.rHalf : (it % 2 == 0 ? R.rOut : R.rIter);
+        };
+        auto rdst = [&](RankState& R, int it) -> double* { return it % 2 == 1 ? R.rOut : R.rIter; };
+        const int aconv = picard(pred_a, [&](size_t lr, int it) {
+          RankState& R = ranks[lr];
+          launch_axial_fast_slab(P, it, d.epsilon, hk, R.i0, R.ni, rsrc(R, it), R.rHalf,
+                                 R.rExpl, rdst(R, it), R.st, stream);
+        }, &r->axial, false);
+        if (aconv < 0) return -aconv;
+        *updates += static_cast<double>(active) * r->axial.iterations;
+        if (aconv > 0) {
+          // accept: Lambda_z[T_new] on the r-slab, r -> z transpose of (T_new, expl)
+          for (size_t lr = 0; lr < ranks.size(); ++lr) {
+            RankState& R = ranks[lr];
+            hA[lr] = rdst(R, aconv);
+            launch_expl_rslab(P, R.i0, R.ni, hA[lr], R.rHalf, R.st, stream);
+            hB[lr] = R.rHalf;
+            dA[lr] = R.zTc;
+            dB[lr] = R.zExpl;
+          }
+          transpose(false, hA.data(), hB.data(), dA.data(), dB.data());
+          r->tau_used = tau;
+          return PCGPU_OK;
+        }
+      }
+      tau *= 0.5;
+      ++r->halvings;
+      if (tau < tau_floor) {
+        err = "time step fell below floor";
+        return PCGPU_ERR_TAU_FLOOR;
+      }
+      r->axial = pcgpu_outcome{};
+    }
+  }
+};
+
+extern "C" {
+
+int pcgpu_nccl_unique_id(void* id128) {
+  std::string e;
+  if (!g_nccl.load(e)) return PCGPU_ERR_CUDA;
+  ncclUniqueId id;
+  if (g_nccl.getUniqueId(&id) != ncclSuccess) return PCGPU_ERR_CUDA;
+  std::memcpy(id128, &id, sizeof id);
+  return PCGPU_OK;
+}
+
+thread_local std::string g_dist_create_error;
+
+int pcgpu_dist_create(const pcgpu_desc* d, int32_t rank, int32_t nranks, const void* nccl_id,
+                      pcgpu_dist** out) {
+  if (!d || !out || nranks < 1) return PCGPU_ERR_ARG;
+  *out = nullptr;
+  std::string v = pcgpu_validate_desc(d);
+  if (v.empty() && d->mode != PCGPU_MODE_FAST)
+    v = "pcgpu_dist: the partitioned stepper runs the fast-mode kernels";
+  if (!v.empty()) {
+    g_dist_create_error = v;
+    return PCGPU_ERR_CONFIG;
+  }
+  auto h = std::make_unique<pcgpu_dist>();
+  try {
+    h->d = *d;
+    h->nranks = nranks;
+    h->local = nccl_id == nullptr;
+    DCK(cudaSetDevice(d->device));
+    DCK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    DCK(cudaEventCreate(&h->ev0));
+    DCK(cudaEventCreate(&h->ev1));
+    build_dev_problem(d, h->P, h->allocs);
+    const int nr = d->nr, nz = d->nz;
+    h->tau_floor = d->tau_min > 0 ? d->tau_min : 1e-12 * d->t_per;
+    for (int i = 0; i < nr; ++i) h->active += (i < d->nr_core ? nz : d->nz_shared);
+    h->zb = split_lines(nz, nranks, [&](int j) { return j < d->nz_shared ? nr : d->nr_core; });
+    h->rb = split_lines(nr, nranks, [&](int i) { return i < d->nr_core ? nz : d->nz_shared; });
+    std::vector<int> mine;
+    if (h->local) {
+      for (int p = 0; p < nranks; ++p) mine.push_back(p);
+    } else {
+      if (rank < 0 || rank >= nranks) throw DistError{PCGPU_ERR_ARG, "pcgpu_dist: bad rank"};
+      mine.push_back(rank);
+      std::string e;
+      if (!g_nccl.load(e)) throw DistError{PCGPU_ERR_CUDA, e};
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof id);
+      NCK(g_nccl.commInitRank(&h->comm, nranks, id, rank));
+    }
+    std::vector<DevStatus*> sts;
+    for (int p : mine) {
+      RankState R;
+      R.rank = p;
+      R.j0 = h->zb[p];
+      R.nj = h->zcount(p);
+      R.i0 = h->rb[p];
+      R.ni = h->rcount(p);
+      const size_t zc = static_cast<size_t>(R.nj) * nr, rc = static_cast<size_t>(R.ni) * nz;
+      R.zTc = h->alloc(zc);
+      R.zExpl = h->alloc(zc);
+      R.zHalf = h->alloc(zc);
+      R.zIter = h->alloc(zc);
+      R.zR = h->alloc(zc);
+      R.rHalf = h->alloc(rc);
+      R.rExpl = h->alloc(rc);
+      R.rOut = h->alloc(rc);
+      R.rIter = h->alloc(rc);
+      // staging: z->r sends 2*zc, receives 2*rc; r->z the reverse
+      R.send = h->alloc(2 * std::max(zc, rc));
+      R.recv = h->alloc(2 * std::max(zc, rc));
+      DevStatus* st = nullptr;
+      DCK(cudaMalloc(&st, sizeof(DevStatus)));
+      h->allocs.push_back(st);
+      R.st = st;
+      sts.push_back(st);
+      h->ranks.push_back(R);
+    }
+    DCK(cudaMalloc(&h->st_dev_list, sizeof(DevStatus*) * sts.size()));
+    h->allocs.push_back(h->st_dev_list);
+    DCK(cudaMemcpy(h->st_dev_list, sts.data(), sizeof(DevStatus*) * sts.size(),
+                   cudaMemcpyHostToDevice));
+    DCK(cudaMallocHost(&h->st_host, sizeof(DevStatus)));
+    DCK(cudaDeviceSynchronize());
+  } catch (const DistError& e) {
+    g_dist_create_error = e.what;
+    return e.code;
+  }
+  *out = h.release();
+  return PCGPU_OK;
+}
+
+void pcgpu_dist_destroy(pcgpu_dist* h) { delete h; }
+
+const char* pcgpu_dist_last_error(const pcgpu_dist* h) {
+  return h ? h->err.c_str() : g_dist_create_error.c_str();
+}
+
+int pcgpu_dist_slabs(const pcgpu_dist* h, int32_t* z0, int32_t* z1, int32_t* r0, int32_t* r1) {
+  // first local rank's slabs (the only one in NCCL mode)
+  const RankState& R = h->ranks[0];
+  *z0 = R.j0;
+  *z1 = R.j0 + R.nj;
+  *r0 = R.i0;
+  *r1 = R.i0 + R.ni;
+  return PCGPU_OK;
+}
+
+// Every rank passes the full initial field (device, N layout). Each rank
+// keeps its z-slab lines and Lambda_z on them (computed on the full field).
+int pcgpu_dist_set_field(pcgpu_dist* h, const double* fieldN) {
+  try {
+    const int nr = h->d.nr, nz = h->d.nz;
+    const size_t cells = static_cast<size_t>(nr) * nz;
+    double *fT = nullptr, *eT = nullptr;
+    DCK(cudaMalloc(&fT, sizeof(double) * cells));
+    DCK(cudaMalloc(&eT, sizeof(double) * cells));
+    transpose_block(fieldN, nr, nz, nr, fT, nz, h->stream);  // N [j][i] -> T [i][j]
+    launch_expl_rslab(h->P, 0, nr, fT, eT, h->ranks[0].st, h->stream);
+    for (RankState& R : h->ranks) {
+      DCK(cudaMemcpyAsync(R.zTc, fieldN + static_cast<size_t>(R.j0) * nr,
+                          sizeof(double) * static_cast<size_t>(R.nj) * nr,
+                          cudaMemcpyDeviceToDevice, h->stream));
+      // Lambda_z of lines Z_r: T-layout columns j0..j0+nj of eT -> N rows
+      transpose_block(eT + R.j0, nz, nr, R.nj, R.zExpl, nr, h->stream);
+    }
+    DCK(cudaStreamSynchronize(h->stream));
+    cudaFree(fT);
+    cudaFree(eT);
+  } catch (const DistError& e) {
+    h->err = e.what;
+    return e.code;
+  }
+  return PCGPU_OK;
+}
+
+// Writes each local rank's z-slab lines into the full-size N-layout buffer.
+int pcgpu_dist_get_field(pcgpu_dist* h, double* fieldN) {
+  try {
+    const int nr = h->d.nr;
+    for (RankState& R : h->ranks)
+      DCK(cudaMemcpyAsync(fieldN + static_cast<size_t>(R.j0) * nr, R.zTc,
+                          sizeof(double) * static_cast<size_t>(R.nj) * nr,
+                          cudaMemcpyDeviceToDevice, h->stream));
+    DCK(cudaStreamSynchronize(h->stream));
+  } catch (const DistError& e) {
+    h->err = e.what;
+    return e.code;
+  }
+  return PCGPU_OK;
+}
+
+int pcgpu_dist_run(pcgpu_dist* h, double t0, int32_t nsteps, pcgpu_step_result* results,
+                   pcgpu_run_stats* stats) {
+  pcgpu_run_stats s{};
+  double t = t0;
+  int rc = PCGPU_OK;
+  try {
+    for (int32_t k = 0; k < nsteps; ++k) {
+      pcgpu_step_result r;
+      double upd = 0;
+      rc = h->step(t, &r, &upd);
+      if (rc) break;
+      t += r.tau_used;
+      if (results) results[k] = r;
+      s.steps += 1;
+      s.halvings += r.halvings;
+      s.radial_iterations += r.radial.iterations;
+      s.axial_iterations += r.axial.iterations;
+      s.cell_updates += upd;
+      s.cell_updates_accepted +=
+          static_cast<double>(h->active) * (r.radial.iterations + r.axial.iterations);
+      s.attempt_cells += 2.0 * static_cast<double>(h->active) * (r.halvings + 1);
+    }
+    DCK(cudaStreamSynchronize(h->stream));
+  } catch (const DistError& e) {
+    h->err = e.what;
+    return e.code;
+  }
+  s.t_end = t;
+  if (stats) *stats = s;
+  return rc;
+}
+
+void* pcgpu_dist_stream(const pcgpu_dist* h) { return h->stream; }
+
+int64_t pcgpu_dist_launch_count(const pcgpu_dist* h) {
+  (void)h;
+  return static_cast<int64_t>(g_launches);
+}
+
+int pcgpu_dist_plan(const pcgpu_desc* d, int32_t nranks, int32_t* zb, int32_t* rb) {
+  if (!d || nranks < 1 || !zb || !rb) return PCGPU_ERR_ARG;
+  const int nr = d->nr, nz = d->nz;
+  const auto z = split_lines(nz, nranks, [&](int j) { return j < d->nz_shared ? nr : d->nr_core; });
+  const auto r = split_lines(nr, nranks, [&](int i) { return i < d->nr_core ? nz : d->nz_shared; });
+  for (int p = 0; p <= nranks; ++p) {
+    zb[p] = z[p];
+    rb[p] = r[p];
+  }
+  return PCGPU_OK;
+}
+
+int pcgpu_dist_enable_timing(pcgpu_dist* h, int32_t on) {
+  h->timing = on != 0;
+  h->transpose_ms = h->radial_ms = h->axial_ms = 0;
+  h->transposes = h->allreduces = h->radial_launches = h->axial_launches = 0;
+  return PCGPU_OK;
+}
+
+int pcgpu_dist_timing(const pcgpu_dist* h, double* transpose_ms, int64_t* transposes,
+                      int64_t* allreduces, double* radial_ms, double* axial_ms) {
+  *transpose_ms = h->transpose_ms;
+  *transposes = h->transposes;
+  *allreduces = h->allreduces;
+  *radial_ms = h->radial_ms;
+  *axial_ms = h->axial_ms;
+  return PCGPU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,130 @@
+"""Partitioned ADI stepper across the B200s of one node.
+
+One process per GPU (torchrun), torch.distributed for the plumbing: rank 0
+creates the NCCL unique id through the library, the process group broadcasts
+it, and every rank builds a `pcgpu_dist` (include/pcgpu.h). The library then
+runs the z-slab radial sweep, the all-to-all transposes and the per-iteration
+allreduce(max) of the Picard norm itself (NCCL on the library's stream).
+With ``emulate=P`` the library runs P virtual ranks in this process on one
+GPU -- the same code path minus NCCL -- which is how the partitioned path is
+validated on a single GPU (bit-identical to the single-GPU fast path).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from . import _native as N
+from .desc import build_desc
+from .errors import ConfigError, DeviceError, TauFloorError
+from .solver import DevicePlan, _step_result
+
+
+def slab_plan(grid, mats, source, timing, cfg, nranks: int) -> Tuple[List[int], List[int]]:
+    """Slab boundaries (host only, no GPU): rank p owns radial lines
+    [zb[p], zb[p+1]) and axial lines [rb[p], rb[p+1])."""
+    lib = N.load()
+    desc, keep = build_desc(grid, mats, source, timing, cfg, N.MODE_FAST, 0)
+    zb = (C.c_int32 * (nranks + 1))()
+    rb = (C.c_int32 * (nranks + 1))()
+    rc = lib.pcgpu_dist_plan(C.byref(desc), nranks, zb, rb)
+    if rc != N.OK:
+        raise ConfigError("pcgpu_dist_plan failed")
+    return list(zb), list(rb)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    if N.load().pcgpu_nccl_unique_id(buf) != N.OK:
+        raise DeviceError("ncclGetUniqueId failed")
+    return bytes(buf)
+
+
+def share_unique_id(rank: int, device=None) -> bytes:
+    """Rank 0 creates the id, torch.distributed broadcasts it."""
+    import torch
+    import torch.distributed as dist
+    backend = dist.get_backend()
+    dev = device if (device is not None and backend == "nccl") else "cpu"
+    t = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        t.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(t, src=0)
+    return bytes(t.cpu().numpy().tobytes())
+
+
+class PartitionedAdi:
+    """z-slab / r-slab partitioned AdiStepper (fast-mode kernels)."""
+
+    def __init__(self, grid, mats, source, timing, cfg, device: int = 0,
+                 rank: int = 0, world: int = 1, emulate: Optional[int] = None,
+                 unique_id: Optional[bytes] = None):
+        self._lib = N.load()
+        cfg.validate()
+        timing.validate()
+        self._grid = grid
+        self._desc, self._keep = build_desc(grid, mats, source, timing, cfg, N.MODE_FAST, device)
+        h = C.c_void_p()
+        if emulate is not None:
+            rc = self._lib.pcgpu_dist_create(C.byref(self._desc), 0, int(emulate), None,
+                                              C.byref(h))
+        else:
+            if unique_id is None:
+                raise ValueError("unique_id required for a multi-process partitioned run")
+            idbuf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+            rc = self._lib.pcgpu_dist_create(C.byref(self._desc), rank, world, idbuf, C.byref(h))
+        if rc != N.OK:
+            msg = self._lib.pcgpu_dist_last_error(None).decode()
+            raise (ConfigError if rc == N.ERR_CONFIG else DeviceError)(msg)
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            self._lib.pcgpu_dist_destroy(self._h)
+            self._h = None
+
+    def _check(self, rc):
+        if rc == N.OK:
+            return
+        msg = self._lib.pcgpu_dist_last_error(self._h).decode()
+        if rc == N.ERR_TAU_FLOOR:
+            raise TauFloorError(msg)
+        raise DeviceError(f"pcgpu_dist error {rc}: {msg}")
+
+    def slabs(self):
+        v = [C.c_int32() for _ in range(4)]
+        self._lib.pcgpu_dist_slabs(self._h, *(C.byref(x) for x in v))
+        return tuple(x.value for x in v)
+
+    def set_field(self, field_dev) -> None:
+        self._check(self._lib.pcgpu_dist_set_field(self._h, C.c_void_p(field_dev.data_ptr())))
+
+    def get_field(self, field_dev) -> None:
+        self._check(self._lib.pcgpu_dist_get_field(self._h, C.c_void_p(field_dev.data_ptr())))
+
+    def run(self, t0: float, nsteps: int, keep_results: bool = False):
+        res = (N.StepResultC * nsteps)() if keep_results and nsteps > 0 else None
+        st = N.RunStats()
+        rc = self._lib.pcgpu_dist_run(self._h, t0, int(nsteps), res, C.byref(st))
+        stats = {k: getattr(st, k) for k, _ in N.RunStats._fields_}
+        self._check(rc)
+        return float(st.t_end), stats, ([_step_result(r) for r in res] if res is not None else [])
+
+    def stream(self) -> int:
+        return int(self._lib.pcgpu_dist_stream(self._h) or 0)
+
+    def launch_count(self) -> int:
+        return int(self._lib.pcgpu_dist_launch_count(self._h))
+
+    def enable_timing(self, on: bool = True) -> None:
+        self._lib.pcgpu_dist_enable_timing(self._h, 1 if on else 0)
+
+    def timing(self) -> dict:
+        tm, rm, am = C.c_double(), C.c_double(), C.c_double()
+        tn, an = C.c_int64(), C.c_int64()
+        self._lib.pcgpu_dist_timing(self._h, C.byref(tm), C.byref(tn), C.byref(an), C.byref(rm),
+                                    C.byref(am))
+        return {"transpose_ms": tm.value, "transposes": tn.value, "allreduces": an.value,
+                "radial_ms": rm.value, "axial_ms": am.value}

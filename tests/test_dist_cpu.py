@@ -1,0 +1,77 @@
+"""Multi-process host logic of the partitioned stepper, world_size 2 over gloo
+(CPU only): every rank computes the same slab plan, the plan tiles both line
+ranges with balanced active cells, and the NCCL unique id created by rank 0
+reaches every rank through torch.distributed."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+from paper_1912_03744_b200 import configs
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1912_03744_b200 import dist as pdist
+        out = {}
+        for name in ("cfg3", "cfg4", "cfg0"):
+            c = configs.CONFIGS[name]()
+            g = c.grid()
+            for nr in (2, 4, 8):
+                zb, rb = pdist.slab_plan(g, c.materials, configs.make_source(c, g), c.timing,
+                                         c.solver, nr)
+                t = torch.tensor(zb + rb, dtype=torch.int64)
+                gathered = [torch.zeros_like(t) for _ in range(world)]
+                dist.all_gather(gathered, t)
+                out[(name, nr)] = [x.tolist() for x in gathered]
+        uid = pdist.share_unique_id(rank)
+        ids = [None] * world
+        dist.all_gather_object(ids, uid)
+        out["ids"] = ids
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_plan_and_unique_id():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    r0 = results[0]
+    assert len(set(r0["ids"])) == 1 and len(r0["ids"][0]) == 128
+    for key, plans in r0.items():
+        if key == "ids":
+            continue
+        assert plans[0] == plans[1], key  # identical plan on every rank
+        name, nr = key
+        c = configs.CONFIGS[name]()
+        g = c.grid()
+        zb, rb = plans[0][: nr + 1], plans[0][nr + 1:]
+        assert zb[0] == 0 and zb[-1] == g.nz() and rb[0] == 0 and rb[-1] == g.nr()
+        assert all(b - a >= 0 for a, b in zip(zb, zb[1:]))
+        # balanced by active cells within one line's worth
+        zc = [sum(g.row_extent(j) for j in range(a, b)) for a, b in zip(zb, zb[1:])]
+        assert max(zc) - min(zc) <= 2 * g.nr()
+        rc = [sum(g.col_extent(i) for i in range(a, b)) for a, b in zip(rb, rb[1:])]
+        assert max(rc) - min(rc) <= 2 * g.nz()

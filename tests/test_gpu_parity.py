@@ -407,3 +407,34 @@ def test_fast_vs_exact_cfg3_full_size(cuda):
     floor = float(((fb - fe).abs() * m).max() / (fe.abs() * m).max())
     print(f"cfg3 fast vs exact {err:.2e}, reference 1-ulp sensitivity {floor:.2e}")
     assert err <= max(FIXED_TOL, 20.0 * floor)
+
+
+# ---------------------------------------------------------------------------
+# Partitioned (multi-GPU) stepper, P ranks emulated in-process on one GPU:
+# bit-identical to the single-GPU fast path.
+@pytest.mark.parametrize("name,nranks,steps", [
+    ("cfg0", 2, 30), ("cfg0", 3, 30), ("cfg4s", 4, 6), ("cfg4s", 8, 6), ("cfg4s", 1, 4),
+])
+def test_partitioned_emulated_bitwise(cuda, name, nranks, steps):
+    import torch
+    from paper_1912_03744_b200.dist import PartitionedAdi
+    case = configs.cfg0() if name == "cfg0" else \
+        configs.scaled(configs.cfg4(), [706, 71, 212, 35], 2048, 1400)
+    g = case.grid()
+    src = configs.make_source(case, g)
+    single = gpu_stepper(case, "fast")
+    f1 = to_dev(make_field(g, case.solver.T0))
+    _, _, r1 = single.run(f1, 0.0, steps, keep_results=True)
+    part = PartitionedAdi(g, case.materials, src, case.timing, case.solver, device=0,
+                          emulate=nranks)
+    f0 = to_dev(make_field(g, case.solver.T0))
+    part.set_field(f0)
+    part.enable_timing(True)
+    _, _, r2 = part.run(0.0, steps, keep_results=True)
+    out = to_dev(make_field(g, 0.0))
+    part.get_field(out)
+    assert _seq(r1).tolist() == _seq(r2).tolist()
+    m = g.mask()
+    assert np.array_equal(to_host(out)[m], to_host(f1)[m])
+    tm = part.timing()
+    assert tm["transposes"] == 2 * steps and tm["allreduces"] > 0
