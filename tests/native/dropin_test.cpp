@@ -1,0 +1,93 @@
+// Drop-in test: the reference's own AdiStepper (compiled from the reference
+// sources) and pulsecell::gpu::AdiStepper (include/pulsecell_gpu) driven
+// side by side on the reference's own objects, in one process; exact mode
+// must agree bit for bit. Built here by tests/native/Makefile (needs the
+// reference headers), run on the GPU box by tests/test_dropin_native.py.
+#include <cstdio>
+#include <cstring>
+
+#include "pulsecell/parallel.hpp"
+#include "pulsecell/solver.hpp"
+#include "pulsecell_gpu/adi_stepper.hpp"
+
+using namespace pulsecell;
+
+int main() {
+  DomainSpec d;
+  d.layer_radii = {1.0e-3, 1.1e-3, 1.4e-3, 1.45e-3};
+  d.core_length = 0.022;
+  d.outer_length = 0.015;
+  d.layer_materials = {"a", "b", "c", "d"};
+  d.source_layer = 2;
+  GridSpec g;
+  g.radial_divisions = {44, 5, 13, 3};
+  g.axial_divisions_core = 128;
+  g.axial_divisions_outer = 87;
+  Grid grid(d, g);
+  MaterialSet set;
+  const double lam0[4] = {400, 0.1, 5, 1}, alpha[4] = {1.5, 1.0, 2.0, 1.0},
+               c0[4] = {1e3, 5e2, 8e2, 6e2};
+  for (int m = 0; m < 4; ++m) {
+    std::vector<Real> kt, cv, lam;
+    for (int k = 4; k <= 300; ++k) {
+      kt.push_back(k);
+      cv.push_back(c0[m] * std::pow(k / 4.2, 3));
+      lam.push_back(lam0[m] * std::pow(k / 4.2, alpha[m]));
+    }
+    PropertyTable chi;
+    if (m == 2) chi = PropertyTable({4.0, 300.0}, {1e-5 * (1 + 0.05 * 4), 1e-5 * (1 + 0.05 * 300)});
+    set.add(MaterialTable(d.layer_materials[m], 1.0, PropertyTable(kt, cv), PropertyTable(kt, lam),
+                          chi));
+  }
+  LayerMaterials layers = resolve_layers(set, d.layer_materials);
+  SourceSpec timing;
+  timing.t_per = 1.0;
+  timing.t_src = 0.3;
+  timing.t_trs = 0.01;
+  timing.I0 = 3.0;
+  timing.S_C = d.source_cross_section();
+  timing.waveform = Waveform::Rectangular;
+  timing.joule_dimensional = true;
+  SolverConfig cfg;
+  cfg.epsilon = 1e-8;
+  cfg.max_iter = 10;
+  cfg.tau_transient_divisor = 1000;
+  cfg.tau_source_divisor = 300;
+  JouleSource src(timing, 2, *layers[2], cfg.range_policy);
+  ExecPlan plan;
+  plan.workers = 4;
+  LinePool pool(plan);
+  pulsecell::AdiStepper cpu(grid, layers, src, timing, cfg, pool);
+  pulsecell::gpu::AdiStepper gpu(grid, layers, src, timing, cfg, {0, true});
+  Array2 fc = make_field(grid, cfg.T0), fg = make_field(grid, cfg.T0);
+  Real t = 0;
+  int bad = 0;
+  for (int k = 0; k < 40; ++k) {
+    const StepResult a = cpu.step(fc, t);
+    const StepResult b = gpu.step(fg, t);
+    if (a.tau_used != b.tau_used || a.halvings != b.halvings ||
+        a.radial.iterations != b.radial.iterations || a.axial.iterations != b.axial.iterations ||
+        a.radial.last_delta != b.radial.last_delta || a.axial.last_delta != b.axial.last_delta)
+      ++bad;
+    t += a.tau_used;
+  }
+  Index diff = 0;
+  for (Index i = 0; i < grid.nr(); ++i)
+    for (Index j = 0; j < grid.col_extent(i); ++j)
+      if (std::memcmp(&fc(i, j), &fg(i, j), sizeof(Real)) != 0) ++diff;
+  // error mapping: max_iter = 1 with a floor above tau0/2 -> TauFloorError
+  SolverConfig c1 = cfg;
+  c1.max_iter = 1;
+  c1.tau_min = 0.9 * initial_tau(0.5, timing, cfg);
+  pulsecell::gpu::AdiStepper g1(grid, layers, src, timing, c1, {0, true});
+  bool threw = false;
+  Array2 f1 = fg;
+  try {
+    g1.step(f1, 0.5);
+  } catch (const TauFloorError&) {
+    threw = true;
+  }
+  std::printf("dropin: steps with mismatching results %d, masked cells differing %ld, "
+              "TauFloorError mapped %s\n", bad, static_cast<long>(diff), threw ? "yes" : "no");
+  return (bad == 0 && diff == 0 && threw) ? 0 : 1;
+}
