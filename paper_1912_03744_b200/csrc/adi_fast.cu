@@ -141,6 +141,30 @@ __device__ __forceinline__ double lean_lookup2(const DevProblem& P, int prop, in
   return __dadd_rn(vs.x, __dmul_rn(Tc - tlo, vs.y));
 }
 
+// Lean v2 lookup: value = a_k + s_k * T on the interval located by
+// x = T / h - t0 / h (one FMA, one conversion, one 16-B load, one FMA).
+// Out-of-range temperatures are rare: a warp vote sends them to the clamp
+// (materials.hpp:40-41) and the clamp_events count (materials.cpp:68).
+__device__ __forceinline__ double lean_v(const DevProblem& P, int prop, int L, double T,
+                                         bool valid) {
+  const double x = fma(T, P.lean_ih[prop], -P.lean_x0[prop]);
+  int k = __double2int_rz(x);
+  k = min(max(k, 0), P.lean_kmax[prop] - 1);
+  const double2 ab = __ldg(reinterpret_cast<const double2*>(P.lean_ab) + P.lean_base[prop] +
+                           L * P.lean_stride[prop] + k + 1);
+  double v = fma(ab.y, T, ab.x);
+  const bool o = !(x >= 0.0 && x <= P.lean_kmaxd[prop]);
+  if (__any_sync(0xffffffffu, o)) {
+    if (o) {
+      const double t0 = P.lean_t0[prop], tK = P.lean_tK[prop];
+      const double Tc = T < t0 ? t0 : (T > tK ? tK : T);
+      v = fma(ab.y, Tc, ab.x);
+      if (valid) atomicAdd(P.clamp + L, 1ull);
+    }
+  }
+  return v;
+}
+
 __device__ __forceinline__ double tile_get(const Tile& t, int e) {
   return *reinterpret_cast<const double*>(reinterpret_cast<const char*>(t.v) + swz(e));
 }
@@ -331,17 +355,17 @@ __global__ void __launch_bounds__(NT, kDirect ? 4 : 3) k_line_fast(DevProblem P,
       int dummy = 0;
       double c;
       if (kAxial) {
-        c = lean_lookup2(P, kLambda, Lax, 0.5 * (tp + ts_c), dummy, false) *
-            __ldg(P.inv_gap_z + min(f, P.nz));
+        c = lean_v(P, kLambda, Lax, 0.5 * (tp + ts_c), false) * __ldg(P.inv_gap_z + min(f, P.nz));
       } else {
         const int Lp = __ldg(P.layer + min(max(f - 1, 0), P.nr - 1));
-        c = lean_lookup2(P, kLambda, Lp, 0.5 * (tp + ts_c), dummy, false) *
-            __ldg(P.gfac_r + min(f, P.nr));
+        c = lean_v(P, kLambda, Lp, 0.5 * (tp + ts_c), false) * __ldg(P.gfac_r + min(f, P.nr));
       }
       fc_lo = vf ? c : 0.0;
       fl_lo = fc_lo * (ta_c - tpa);
     }
     double cp_prev = 0.0, up_prev = 0.0, vp_prev = 0.0;
+    const double2* met = reinterpret_cast<const double2*>(kAxial ? P.zmet : P.rmet);
+    const int nmet = kAxial ? P.nz : P.nr;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       const int i = s + k;
@@ -349,49 +373,39 @@ __global__ void __launch_bounds__(NT, kDirect ? 4 : 3) k_line_fast(DevProblem P,
       const int f = i + 1;  // face between rows i and i+1
       const bool vf = f <= nm1;
       const bool vi = i < n;
+      // per-row metrics {face conductance factor of face i+1, 1/control volume of row i}
+      const double2 mt = __ldg(met + min(i, nmet - 1));
       int Ln = Lc;
-      double c;
+      double lam;
       if (kAxial) {
-        c = lean_lookup2(P, kLambda, Lax, 0.5 * (ts_c + ts_n), oor, vf) *
-            __ldg(P.inv_gap_z + min(f, P.nz));
+        lam = lean_v(P, kLambda, Lax, 0.5 * (ts_c + ts_n), vf);
       } else {
         Ln = __ldg(P.layer + min(f, P.nr - 1));
-        int o = 0;
-        c = lean_lookup2(P, kLambda, Lc, 0.5 * (ts_c + ts_n), o, vf) *
-            __ldg(P.gfac_r + min(f, P.nr));
-        if (o) atomicAdd(P.clamp + Lc, 1ull);
+        lam = lean_v(P, kLambda, Lc, 0.5 * (ts_c + ts_n), vf);
       }
-      const double fc_hi = vf ? c : 0.0;
+      const double fc_hi = vf ? lam * mt.x : 0.0;
       const double fl_hi = fc_hi * (ta_n - ta_c);
       const double exk = ld_ex(k);
-      double Ak, Ck, bk, dk;
+      const double inv = mt.y;  // inv_eta (axial) / inv_vol (radial)
+      double Ak = fc_lo * inv, Ck = fc_hi * inv, bk, dk;
       if (kAxial) {
-        const double inv_eta = __ldg(P.inv_eta + min(i, P.nz - 1));
-        Ak = fc_lo * inv_eta;
-        Ck = fc_hi * inv_eta;
-        const double K = rho_hk_ax * lean_lookup2(P, kCv, Lax, ta_c, oor, vi);
+        const double K = A.hk * lean_v(P, kCv, Lax, ta_c, vi);  // rho folded in
         bk = K + Ak + Ck;
-        // terminal face: face_top is nonzero only on Dirichlet lines
-        const bool top = i == nm1;
-        bk += top ? face_top * inv_eta : 0.0;
+        const bool top = i == nm1;  // terminal Dirichlet face (face_top = 0 elsewhere)
+        bk += top ? face_top * inv : 0.0;
         const double fh = fl_hi + (top ? face_top * (P.T0 - ta_c) : 0.0);
-        dk = exk + (fh - fl_lo) * inv_eta;
+        dk = exk + (fh - fl_lo) * inv;
       } else {
-        const double inv_vol = __ldg(P.inv_vol_r + min(i, P.nr - 1));
-        Ak = fc_lo * inv_vol;
-        Ck = fc_hi * inv_vol;
-        int o = 0;
-        const double K = P.lean_rho[Lc] * A.hk * lean_lookup2(P, kCv, Lc, ts_c, o, vi);
+        const double K = A.hk * lean_v(P, kCv, Lc, ts_c, vi);  // rho folded in
         double src = 0.0;
         if (kLean == 2) {
           // JouleSource::power: chi(T) * amplitude * pulse in the source layer
           const bool on = Lc == P.source_layer;
           src = (on ? src_amp : 0.0) *
-                lean_lookup2(P, kChi, P.source_layer, ts_c, o, vi && on && src_amp != 0.0);
+                lean_v(P, kChi, P.source_layer, ts_c, vi && on && src_amp != 0.0);
         }
-        if (o) atomicAdd(P.clamp + Lc, static_cast<unsigned long long>(o));
         bk = K + Ak + Ck;
-        dk = (fl_hi - fl_lo) * inv_vol + exk + src;
+        dk = (fl_hi - fl_lo) * inv + exk + src;
       }
       Ak = vi ? Ak : 0.0;
       Ck = vi ? Ck : 0.0;

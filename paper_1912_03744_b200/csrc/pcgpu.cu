@@ -540,7 +540,7 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
     }
     if (d->source_kind == PCGPU_SOURCE_JOULE && P.mats[d->source_layer].n[2] == 0) P.lean = 0;
     if (std::getenv("PCGPU_NO_LEAN")) P.lean = 0;
-    std::vector<double> lt;  // lean table, uploaded below
+    std::vector<double> lt, lab;  // lean tables, uploaded below
     if (P.lean) {
       // property-grouped lean table: (prop, layer, k) -> {v[k-1], slope_k}
       for (int p = 0; p < 3; ++p) {
@@ -555,15 +555,27 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
         P.lean_tK[p] = ref >= 0 ? P.mats[ref].t_last[p] : 0.0;
         P.lean_inv_h[p] = ref >= 0 ? P.mats[ref].inv_h[p] : 0.0;
         P.lean_h[p] = P.lean_inv_h[p] > 0.0 ? 1.0 / P.lean_inv_h[p] : 0.0;
+        if (ref >= 0) {
+          const double t0 = P.mats[ref].t_first[p], tK = P.mats[ref].t_last[p];
+          P.lean_ih[p] = (n - 1) / (tK - t0);
+          P.lean_x0[p] = t0 * P.lean_ih[p];
+          P.lean_kmaxd[p] = n - 1;
+        }
         for (int m = 0; m < d->n_layers; ++m) {
+          const double scale = p == 0 ? d->materials[m].rho : 1.0;  // rho folded into c_V
           for (int k = 0; k < n; ++k) {
             if (P.mats[m].n[p] == n && k >= 1) {
               const int o = P.mats[m].off[p] + k;
               lt.push_back(vals[o - 1]);
               lt.push_back(slopes[o]);
+              const double sl = slopes[o];
+              lab.push_back(scale * (vals[o - 1] - sl * knots[o - 1]));
+              lab.push_back(scale * sl);
             } else {
               lt.push_back(0.0);
               lt.push_back(0.0);
+              lab.push_back(0.0);
+              lab.push_back(0.0);
             }
           }
         }
@@ -596,7 +608,21 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
     P.knots = up(knots);
     P.vals = up(vals);
     P.slopes = up(slopes);
-    if (P.lean) P.lean_tab = up(lt);
+    if (P.lean) {
+      P.lean_tab = up(lt);
+      P.lean_ab = up(lab);
+      std::vector<double> rm(2 * static_cast<size_t>(nr)), zm(2 * static_cast<size_t>(nz));
+      for (int i = 0; i < nr; ++i) {
+        rm[2 * i] = i + 1 < nr ? face_r_lo[i + 1] * inv_gap_r[i + 1] : 0.0;
+        rm[2 * i + 1] = inv_vol_r[i];
+      }
+      for (int j = 0; j < nz; ++j) {
+        zm[2 * j] = inv_gap_z[j + 1];
+        zm[2 * j + 1] = inv_eta[j];
+      }
+      P.rmet = up(rm);
+      P.zmet = up(zm);
+    }
     P.ivl = up(ivl);
     P.source_kind = d->source_kind;
     P.source_layer = d->source_layer;
