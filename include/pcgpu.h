@@ -206,6 +206,16 @@ int pcgpu_axial_half_step_host(pcgpu_stepper* h, const double* T_half_host, doub
 int pcgpu_run(pcgpu_stepper* h, double* field, double t0, int32_t nsteps,
               pcgpu_step_result* results, pcgpu_run_stats* stats);
 
+/* The BASELINE adaptive policy (configs[2]/[4]) above step(): start at
+ * tau_start, halve on non-convergence exactly like step() (solver.cpp:369-371),
+ * grow by `grow` after `easy_steps` consecutive steps accepted without
+ * halving, never above tau_max; stop at t_end or after max_steps. Not in the
+ * reference (halving only); the CPU oracle implements the same
+ * policy (oracle_run_growth) so both paths take identical decisions. */
+int pcgpu_run_growth(pcgpu_stepper* h, double* field, double t0, double t_end, int32_t max_steps,
+                     double tau_start, double grow, int32_t easy_steps, double tau_max,
+                     pcgpu_step_result* results, pcgpu_run_stats* stats);
+
 /* MaterialTable::clamp_events() per layer (materials.hpp:85, materials.cpp:68).
  * counts has n_layers entries. Counted per out-of-range evaluation on the device. */
 int pcgpu_clamp_events(const pcgpu_stepper* h, uint64_t* counts);

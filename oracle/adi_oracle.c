@@ -511,9 +511,15 @@ int oracle_axial_half_step(oracle* o, const double* T_half, double t, double tau
 }
 
 /* ---- solver.cpp:356-373 step: tau controller ---------------------------- */
+static int step_tau(oracle* o, double* field, double t, double tau, pcgpu_step_result* res);
+
 int oracle_step(oracle* o, double* field, double t, pcgpu_step_result* res) {
+  return step_tau(o, field, t, oracle_initial_tau(o, t), res);
+}
+
+/* solver.cpp:356-373 with the first tau supplied by the caller. */
+static int step_tau(oracle* o, double* field, double t, double tau, pcgpu_step_result* res) {
   const size_t bytes = sizeof(double) * (size_t)o->nr * o->nz;
-  double tau = oracle_initial_tau(o, t);
   memset(res, 0, sizeof *res);
   for (;;) {
     int rc = oracle_radial_half_step(o, field, t, tau, o->half, &res->radial);
@@ -563,6 +569,42 @@ int oracle_run(oracle* o, double* field, double t0, int32_t nsteps, pcgpu_step_r
     st.axial_iterations += r.axial.iterations;
     st.cell_updates_accepted += cells * (r.radial.iterations + r.axial.iterations);
     st.attempt_cells += 2.0 * cells;
+  }
+  st.t_end = t;
+  st.cell_updates = st.cell_updates_accepted;
+  if (stats) *stats = st;
+  return rc;
+}
+
+/* The BASELINE growth policy (see pcgpu_run_growth in include/pcgpu.h): the
+ * same controller over the same step semantics, so the GPU and the oracle
+ * take identical decisions on identical results. */
+int oracle_run_growth(oracle* o, double* field, double t0, double t_end, int32_t max_steps,
+                      double tau_start, double grow, int32_t easy_steps, double tau_max,
+                      pcgpu_step_result* results, pcgpu_run_stats* stats) {
+  pcgpu_run_stats st;
+  memset(&st, 0, sizeof st);
+  double cells = 0;
+  for (int i = 0; i < o->nr; ++i) cells += col_extent(o, i);
+  double t = t0, tau = tau_start < tau_max ? tau_start : tau_max;
+  int easy = 0, rc = PCGPU_OK;
+  for (int32_t k = 0; k < max_steps && t < t_end; ++k) {
+    pcgpu_step_result r;
+    rc = step_tau(o, field, t, tau, &r);
+    if (rc) break;
+    t += r.tau_used;
+    if (results) results[k] = r;
+    st.steps += 1;
+    st.halvings += r.halvings;
+    st.radial_iterations += r.radial.iterations;
+    st.axial_iterations += r.axial.iterations;
+    st.cell_updates_accepted += cells * (r.radial.iterations + r.axial.iterations);
+    tau = r.tau_used;
+    easy = r.halvings == 0 ? easy + 1 : 0;
+    if (easy >= easy_steps) {
+      tau = tau * grow < tau_max ? tau * grow : tau_max;
+      easy = 0;
+    }
   }
   st.t_end = t;
   st.cell_updates = st.cell_updates_accepted;

@@ -32,6 +32,9 @@ int oracle_axial_half_step(oracle* o, const double* T_half, double t, double tau
 int oracle_step(oracle* o, double* field, double t, pcgpu_step_result* res);
 int oracle_run(oracle* o, double* field, double t0, int32_t nsteps, pcgpu_step_result* results,
                pcgpu_run_stats* stats);
+int oracle_run_growth(oracle* o, double* field, double t0, double t_end, int32_t max_steps,
+                      double tau_start, double grow, int32_t easy_steps, double tau_max,
+                      pcgpu_step_result* results, pcgpu_run_stats* stats);
 int oracle_clamp_events(const oracle* o, uint64_t* counts);
 /* thomas_solve_inplace (tridiagonal.hpp:25-42); returns PCGPU_ERR_ZERO_PIVOT. */
 int oracle_thomas(const double* lower, const double* diag, const double* upper,

@@ -76,6 +76,9 @@ def _load_port():
             ("oracle_step", C.c_int, [_vp, _vp, C.c_double, S]),
             ("oracle_run", C.c_int, [_vp, _vp, C.c_double, C.c_int32, S, R]),
             ("oracle_clamp_events", C.c_int, [_vp, C.POINTER(C.c_uint64)]),
+            ("oracle_run_growth", C.c_int, [_vp, _vp, C.c_double, C.c_double, C.c_int32,
+                                            C.c_double, C.c_double, C.c_int32, C.c_double, S,
+                                            R]),
             ("oracle_thomas", C.c_int, [_vp] * 6 + [C.c_int64]),
             ("oracle_thomas_batch", C.c_int, [_vp] * 5 + [C.c_int64, C.c_int64, C.c_int32,
                                                           C.POINTER(C.c_int64)]),
@@ -194,6 +197,18 @@ class OracleError(RuntimeError):
 class PortStepper(_Base):
     """The C restatement, driven by the same descriptor as the GPU library."""
     prefix = "oracle_"
+
+    def run_growth(self, field, t0, t_end, max_steps, policy=None):
+        from paper_1912_03744_b200.solver import GrowthPolicy
+        pol = policy or GrowthPolicy()
+        res = (N.StepResultC * max(1, max_steps))()
+        st = N.RunStats()
+        rc = self.lib.oracle_run_growth(self.h, _ptr(field), t0, t_end, int(max_steps),
+                                        pol.tau_start, pol.grow, int(pol.easy_steps),
+                                        pol.tau_max, res, C.byref(st))
+        stats = {k: getattr(st, k) for k, _ in N.RunStats._fields_}
+        self._check(rc)
+        return float(st.t_end), stats, [_result(res[k]) for k in range(int(st.steps))]
 
     def __init__(self, case, source_kind=None):
         from paper_1912_03744_b200.source import FieldSource, JouleSource, NullSource

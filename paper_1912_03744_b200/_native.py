@@ -79,7 +79,7 @@ EXPORTS = [
     "pcgpu_tridiag_batch", "pcgpu_nccl_unique_id", "pcgpu_dist_create", "pcgpu_dist_destroy",
     "pcgpu_dist_last_error", "pcgpu_dist_plan", "pcgpu_dist_slabs", "pcgpu_dist_set_field",
     "pcgpu_dist_get_field", "pcgpu_dist_run", "pcgpu_dist_stream", "pcgpu_dist_enable_timing",
-    "pcgpu_dist_timing", "pcgpu_dist_launch_count",
+    "pcgpu_dist_timing", "pcgpu_dist_launch_count", "pcgpu_run_growth",
 ]
 
 _lib = None
@@ -120,6 +120,9 @@ def load():
         "pcgpu_run": (C.c_int, [vp, vp, C.c_double, C.c_int32, C.POINTER(StepResultC),
                                 C.POINTER(RunStats)]),
         "pcgpu_clamp_events": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
+        "pcgpu_run_growth": (C.c_int, [vp, vp, C.c_double, C.c_double, C.c_int32, C.c_double,
+                                       C.c_double, C.c_int32, C.c_double,
+                                       C.POINTER(StepResultC), C.POINTER(RunStats)]),
         "pcgpu_stream": (vp, [vp]),
         "pcgpu_kernel_timing": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                           C.POINTER(C.c_double), C.POINTER(C.c_int64)]),

@@ -400,8 +400,8 @@ struct pcgpu_stepper {
   // step(): tau controller (solver.cpp:356-373). `field` is N layout; on
   // acceptance *accepted holds the N-layout buffer with the new field.
   int step(const double* field, double t, double* next, const double** accepted,
-           pcgpu_step_result* r, double* attempt_updates) {
-    double tau = host_initial_tau(d, t);
+           pcgpu_step_result* r, double* attempt_updates, double tau0 = -1.0) {
+    double tau = tau0 > 0 ? tau0 : host_initial_tau(d, t);
     std::memset(r, 0, sizeof *r);
     for (;;) {
       const double* half = nullptr;
@@ -836,6 +836,65 @@ int pcgpu_run(pcgpu_stepper* h, double* field, double t0, int32_t nsteps,
       nxt = old;
     } else {
       spare = old;
+    }
+  }
+  h->buf[kField] = cur;
+  h->buf[kNext] = nxt;
+  h->buf[kIterT] = spare;
+  h->from_state(cur, field);
+  CK(cudaStreamSynchronize(h->stream));
+  GUARD_END(h)
+  s.t_end = t;
+  if (stats) *stats = s;
+  return rc;
+}
+
+// The BASELINE adaptive policy (configs[2], configs[4]) as a controller
+// above step(): start at tau_start; a step that needs halving (a Picard sweep
+// did not converge within max_iter) retries at tau/2 like the reference
+// (solver.cpp:369-371); after `easy_steps` consecutive steps accepted without
+// halving, tau grows by `grow`; tau never exceeds tau_max. The reference has
+// no growth logic; the policy is shared with the CPU oracle so
+// both see the same decisions.
+int pcgpu_run_growth(pcgpu_stepper* h, double* field, double t0, double t_end, int32_t max_steps,
+                     double tau_start, double grow, int32_t easy_steps, double tau_max,
+                     pcgpu_step_result* results, pcgpu_run_stats* stats) {
+  if (!h || !field || max_steps < 0 || !(tau_start > 0) || !(grow >= 1.0)) return PCGPU_ERR_ARG;
+  pcgpu_run_stats s{};
+  double t = t0, tau = std::min(tau_start, tau_max);
+  int easy = 0, rc = PCGPU_OK;
+  GUARD_BEGIN
+  double* cur = h->buf[kField];
+  double* nxt = h->buf[kNext];
+  double* spare = h->buf[kIterT];
+  h->to_state(field, cur);
+  for (int32_t k = 0; k < max_steps && t < t_end; ++k) {
+    pcgpu_step_result r;
+    const double* acc = nullptr;
+    double upd = 0;
+    h->buf[kIterT] = spare;
+    rc = h->step(cur, t, nxt, &acc, &r, &upd, tau);
+    if (rc) break;
+    t += r.tau_used;
+    if (results) results[k] = r;
+    s.steps += 1;
+    s.halvings += r.halvings;
+    s.radial_iterations += r.radial.iterations;
+    s.axial_iterations += r.axial.iterations;
+    s.cell_updates += upd;
+    s.cell_updates_accepted +=
+        static_cast<double>(h->active) * (r.radial.iterations + r.axial.iterations);
+    s.attempt_cells += 2.0 * static_cast<double>(h->active) * (r.halvings + 1);
+    double* accepted = const_cast<double*>(acc);
+    double* old = cur;
+    cur = accepted;
+    if (accepted == nxt) nxt = old; else spare = old;
+    // controller: carry the accepted tau, grow after `easy_steps` easy steps
+    tau = r.tau_used;
+    easy = r.halvings == 0 ? easy + 1 : 0;
+    if (easy >= easy_steps) {
+      tau = std::min(tau * grow, tau_max);
+      easy = 0;
     }
   }
   h->buf[kField] = cur;

@@ -73,6 +73,19 @@ def make_field(grid: Grid, value: float) -> np.ndarray:
 
 
 @dataclass
+class GrowthPolicy:
+    """BASELINE.json adaptive dt (configs[2], configs[4]): start at 1e-5 s, halve
+    when Picard does not converge within max_iter (the reference's own halving,
+    solver.cpp:369-371), grow x1.2 after 5 easy steps (accepted without
+    halving), cap at 1e-3 s. Not in the reference; the same
+    policy runs in the CPU oracle (oracle_run_growth)."""
+    tau_start: float = 1e-5
+    grow: float = 1.2
+    easy_steps: int = 5
+    tau_max: float = 1e-3
+
+
+@dataclass
 class HalfStepOutcome:  # solver.hpp:50-54
     converged: bool = False
     iterations: int = 0
@@ -248,6 +261,25 @@ class AdiStepper:
         stats = {k: getattr(st, k) for k, _ in N.RunStats._fields_}
         self._check(rc)
         results = [_step_result(r) for r in res] if res is not None else []
+        return float(st.t_end), stats, results
+
+    def run_growth(self, fld, t0: float, t_end: float, max_steps: int,
+                   policy: Optional["GrowthPolicy"] = None, keep_results: bool = False):
+        """Run under the BASELINE growth policy (device field); returns
+        (t_end, stats, [StepResult])."""
+        pol = policy or GrowthPolicy()
+        p, dev = self._field(fld, True)
+        if not dev:
+            raise ValueError("run_growth() takes a device field (torch CUDA tensor)")
+        res = (N.StepResultC * max_steps)() if keep_results and max_steps > 0 else None
+        st = N.RunStats()
+        rc = self._lib.pcgpu_run_growth(self._h, C.c_void_p(p), t0, t_end, int(max_steps),
+                                        pol.tau_start, pol.grow, int(pol.easy_steps),
+                                        pol.tau_max, res, C.byref(st))
+        stats = {k: getattr(st, k) for k, _ in N.RunStats._fields_}
+        self._check(rc)
+        n = int(st.steps)
+        results = [_step_result(res[k]) for k in range(n)] if res is not None else []
         return float(st.t_end), stats, results
 
     def clamp_events(self) -> List[int]:

@@ -438,3 +438,30 @@ def test_partitioned_emulated_bitwise(cuda, name, nranks, steps):
     assert np.array_equal(to_host(out)[m], to_host(f1)[m])
     tm = part.timing()
     assert tm["transposes"] == 2 * steps and tm["allreduces"] > 0
+
+
+# ---------------------------------------------------------------------------
+# BASELINE growth controller (configs[2]/[4]): identical decisions on GPU and
+# the oracle; exact mode bitwise, fast mode identical sequences.
+@pytest.mark.parametrize("name", ["cfg2s", "cfg4s"])
+def test_growth_controller_matches_oracle(cuda, name):
+    from paper_1912_03744_b200.solver import GrowthPolicy
+    base = configs.cfg2() if name == "cfg2s" else configs.cfg4()
+    case = configs.scaled(base, [44, 5, 13, 3], 128, 87 if name == "cfg4s" else 128)
+    g = case.grid()
+    pol = GrowthPolicy()
+    port = PortStepper(case)
+    fo = make_field(g, case.solver.T0)
+    t_o, st_o, res_o = port.run_growth(fo, 0.0, 0.35, 400, pol)
+    assert st_o["steps"] > 50 and max(r.tau_used for r in res_o) > 1e-4  # it grew
+    for mode in ("exact", "fast"):
+        gpu = gpu_stepper(case, mode)
+        fg = to_dev(make_field(g, case.solver.T0))
+        t_g, st_g, res_g = gpu.run_growth(fg, 0.0, 0.35, 400, pol, keep_results=True)
+        sg, so = _seq(res_g), _seq(res_o)
+        assert np.array_equal(sg[:, :4], so[:, :4])  # accepted dt, halvings, iterations
+        if mode == "exact":
+            assert t_g == t_o and np.array_equal(sg, so)
+            assert np.array_equal(to_host(fg)[g.mask()], fo[g.mask()])
+        else:
+            assert _rel(to_host(fg), fo, g.mask()) <= ADAPTIVE_TOL
