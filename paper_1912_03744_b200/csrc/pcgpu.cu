@@ -488,10 +488,12 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
           P.mats[m].v_first[p] = t.v[0];
           P.mats[m].v_last[p] = t.v[t.n - 1];
         }
+        P.mats[m].xmode[p] = 0;
         if (t.n == 2) {
           // a single interval: the bracket is always k = 1
           P.mats[m].uniform[p] = 2;
           P.mats[m].inv_h[p] = 0.0;
+          P.mats[m].xmode[p] = 2;
         } else if (t.n >= 3) {
           // Uniform-knot bracket guess (exactness is kept by the device fix-up).
           const double inv_h = (t.n - 1) / (t.t[t.n - 1] - t.t[0]);
@@ -511,6 +513,7 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
             if (exact) {
               P.mats[m].uniform[p] = 2;
               P.mats[m].inv_h[p] = 1.0 / h;
+              P.mats[m].xmode[p] = 1;
             }
           }
         }
@@ -540,6 +543,22 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
     }
     if (d->source_kind == PCGPU_SOURCE_JOULE && P.mats[d->source_layer].n[2] == 0) P.lean = 0;
     if (std::getenv("PCGPU_NO_LEAN")) P.lean = 0;
+    // exact kernels' branch-free lookups: lambda/cv tables xmode 1 whose t0 >= 0
+    // is a multiple of h and whose top knot's ulp is below h (T - t0 exact), chi
+    // a single interval or absent; MeanTemperature faces.
+    P.exact_x = d->halfpoint_rule == PCGPU_HALFPOINT_MEAN_TEMPERATURE;
+    for (int m = 0; m < d->n_layers && P.exact_x; ++m) {
+      for (int p = 0; p < 2; ++p) {
+        const DevMaterial& dm = P.mats[m];
+        if (dm.xmode[p] != 1) { P.exact_x = 0; break; }
+        const double h = 1.0 / dm.inv_h[p];
+        const double q = dm.t_first[p] / h;
+        if (dm.t_first[p] < 0 || q != std::floor(q) || std::nextafter(dm.t_last[p], 1e300) - dm.t_last[p] > h)
+          P.exact_x = 0;
+      }
+      if (P.mats[m].n[2] > 0 && P.mats[m].xmode[2] != 2) P.exact_x = 0;
+    }
+    if (std::getenv("PCGPU_NO_EXACTX")) P.exact_x = 0;
     std::vector<double> lt, lab;  // lean tables, uploaded below
     if (P.lean) {
       // property-grouped lean table: (prop, layer, k) -> {v[k-1], slope_k}
