@@ -514,6 +514,7 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
               P.mats[m].uniform[p] = 2;
               P.mats[m].inv_h[p] = 1.0 / h;
               P.mats[m].xmode[p] = 1;
+              P.mats[m].h[p] = h;
             }
           }
         }
@@ -551,7 +552,7 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
       for (int p = 0; p < 2; ++p) {
         const DevMaterial& dm = P.mats[m];
         if (dm.xmode[p] != 1) { P.exact_x = 0; break; }
-        const double h = 1.0 / dm.inv_h[p];
+        const double h = dm.h[p];
         const double q = dm.t_first[p] / h;
         if (dm.t_first[p] < 0 || q != std::floor(q) || std::nextafter(dm.t_last[p], 1e300) - dm.t_last[p] > h)
           P.exact_x = 0;
@@ -559,6 +560,7 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
       if (P.mats[m].n[2] > 0 && P.mats[m].xmode[2] != 2) P.exact_x = 0;
     }
     if (std::getenv("PCGPU_NO_EXACTX")) P.exact_x = 0;
+    P.exact_ws = std::getenv("PCGPU_NO_EXACTWS") ? 0 : 1;
     std::vector<double> lt, lab;  // lean tables, uploaded below
     if (P.lean) {
       // property-grouped lean table: (prop, layer, k) -> {v[k-1], slope_k}
