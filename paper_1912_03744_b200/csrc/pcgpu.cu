@@ -458,7 +458,7 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
     std::vector<int> layer(d->layer, d->layer + nr);
 
     // Tables, flattened.
-    std::vector<double> knots, vals, slopes, ivl;
+    std::vector<double> knots, vals, slopes, ivl, xpair;
     
     P.n_layers = d->n_layers;
     for (int m = 0; m < d->n_layers; ++m) {
@@ -481,6 +481,8 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
           ivl.push_back(t.t[k]);
           ivl.push_back(k == 0 ? t.v[0] : t.v[k - 1]);
           ivl.push_back(sl);
+          xpair.push_back(t.v[k]);
+          xpair.push_back(k + 1 < t.n ? t.v[k + 1] - t.v[k] : 0.0);
         }
         if (t.n > 0) {
           P.mats[m].t_first[p] = t.t[0];
@@ -645,6 +647,7 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
       P.zmet = up(zm);
     }
     P.ivl = up(ivl);
+    P.xpair = up(xpair);
     P.source_kind = d->source_kind;
     P.source_layer = d->source_layer;
     P.amplitude = d->amplitude;
