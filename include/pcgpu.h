@@ -230,6 +230,10 @@ int pcgpu_kernel_timing(const pcgpu_stepper* h, double* radial_ms, int64_t* radi
 int pcgpu_enable_kernel_timing(pcgpu_stepper* h, int32_t on);
 /* Number of this library's kernels launched since creation. */
 int64_t pcgpu_launch_count(const pcgpu_stepper* h);
+/* The kernel variants this stepper selected, as text (e.g.
+ * "mode=exact lines=ws lookups=exact-x"), into buf (NUL-terminated, at most
+ * len bytes). Returns the full length. */
+int32_t pcgpu_describe(const pcgpu_stepper* h, char* buf, int32_t len);
 
 /* ---- Partitioned stepper: one node of B200s ------------------
  * z-slabs (radial lines j) for the radial sweep, r-slabs (axial lines i) for

@@ -79,7 +79,7 @@ EXPORTS = [
     "pcgpu_tridiag_batch", "pcgpu_nccl_unique_id", "pcgpu_dist_create", "pcgpu_dist_destroy",
     "pcgpu_dist_last_error", "pcgpu_dist_plan", "pcgpu_dist_slabs", "pcgpu_dist_set_field",
     "pcgpu_dist_get_field", "pcgpu_dist_run", "pcgpu_dist_stream", "pcgpu_dist_enable_timing",
-    "pcgpu_dist_timing", "pcgpu_dist_launch_count", "pcgpu_run_growth",
+    "pcgpu_dist_timing", "pcgpu_dist_launch_count", "pcgpu_run_growth", "pcgpu_describe",
 ]
 
 _lib = None
@@ -128,6 +128,7 @@ def load():
                                           C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
         "pcgpu_enable_kernel_timing": (C.c_int, [vp, C.c_int32]),
         "pcgpu_launch_count": (C.c_int64, [vp]),
+        "pcgpu_describe": (C.c_int32, [vp, C.c_char_p, C.c_int32]),
         "pcgpu_tridiag_batch": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, C.c_int64, C.c_int32,
                                           C.c_int32, vp, C.POINTER(C.c_int64)]),
         "pcgpu_nccl_unique_id": (C.c_int, [vp]),

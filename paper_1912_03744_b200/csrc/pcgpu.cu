@@ -749,6 +749,25 @@ int64_t pcgpu_launch_count(const pcgpu_stepper* h) {
   return static_cast<int64_t>(g_launches - h->launches0);
 }
 
+int32_t pcgpu_describe(const pcgpu_stepper* h, char* buf, int32_t len) {
+  std::string s;
+  if (h->d.mode == PCGPU_MODE_EXACT) {
+    s = "mode=exact lines=";
+    s += h->P.exact_ws ? "ws" : "thread";
+    s += " lookups=";
+    s += h->P.exact_x ? "exact-x" : "generic";
+  } else {
+    s = "mode=fast lookups=";
+    s += h->P.lean ? "lean" : (h->P.all_u2 ? "u2" : "generic");
+  }
+  if (buf && len > 0) {
+    const size_t n = std::min(s.size(), static_cast<size_t>(len - 1));
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+  return static_cast<int32_t>(s.size());
+}
+
 int pcgpu_bind_power_field(pcgpu_stepper* h, const double* power_dev) {
   if (h->d.source_kind != PCGPU_SOURCE_FIELD || !power_dev)
     return h->fail(PCGPU_ERR_ARG, "bind_power_field: source kind is not FIELD");

@@ -311,3 +311,9 @@ class AdiStepper:
 
     def launch_count(self) -> int:
         return int(self._lib.pcgpu_launch_count(self._h))
+
+    def describe(self) -> str:
+        """The kernel variants the library selected for this problem."""
+        buf = C.create_string_buffer(256)
+        self._lib.pcgpu_describe(self._h, buf, 256)
+        return buf.value.decode()

@@ -465,3 +465,58 @@ def test_growth_controller_matches_oracle(cuda, name):
             assert np.array_equal(to_host(fg)[g.mask()], fo[g.mask()])
         else:
             assert _rel(to_host(fg), fo, g.mask()) <= ADAPTIVE_TOL
+
+
+# ---- exact mode on the kernel variants the large configs select -------------
+def _cfg4s():
+    return configs.scaled(configs.cfg4(), [44, 5, 13, 3], 128, 87)
+
+
+def test_exact_selects_ws_and_exact_x_for_configs(cuda):
+    gpu = gpu_stepper(_cfg4s(), "exact")
+    assert gpu.describe() == "mode=exact lines=ws lookups=exact-x"
+    gpu = gpu_stepper(configs.step_cell(True), "exact")
+    assert gpu.describe().startswith("mode=exact lines=ws")
+
+
+def test_exact_x_out_of_range_clamp_events_bitwise(cuda):
+    """Cells below the power-law tables (4..300 K) in every layer: clamp events
+    are counted per layer exactly as the reference counts them, and the fields
+    stay bit-identical. (A hot spot above 300 K in a 4.2 K cell makes the
+    reference itself fail its tau floor, so only the lower clamp is driven.)"""
+    case = _cfg4s()
+    g = case.grid()
+    f = make_field(g, case.solver.T0)
+    f[10:12, 20:23] = 3.9
+    f[46, 30:32] = 3.95
+    f[50:52, 5:7] = 3.95
+    f[63, 40] = 3.97
+    port, gpu = PortStepper(case), gpu_stepper(case, "exact")
+    fo = f.copy(order="F")
+    te_o, _, res_o = port.run(fo, 0.0, 6)
+    fg = to_dev(f)
+    te_g, _, res_g = gpu.run(fg, 0.0, 6, keep_results=True)
+    assert te_g == te_o
+    assert np.array_equal(_seq(res_g), _seq(res_o))
+    m = g.mask()
+    assert np.array_equal(to_host(fg)[m], fo[m])
+    assert gpu.clamp_events() == port.clamp_events()
+    assert sum(port.clamp_events()) > 0
+    assert sum(1 for c in port.clamp_events() if c) >= 2
+
+
+def test_exact_x_strict_range_lowest_line(cuda):
+    case = _cfg4s()
+    case.solver.range_policy = RangePolicy.Strict
+    g = case.grid()
+    f = make_field(g, case.solver.T0)
+    f[40, 70] = 500.0
+    f[20, 12] = 1.0
+    port, gpu = PortStepper(case), gpu_stepper(case, "exact")
+    for half in ("radial_half_step", "axial_half_step"):
+        with pytest.raises(OracleError) as eo:
+            getattr(port, half)(f, 0.0, 1e-4, make_field(g, 0.0))
+        with pytest.raises(LineError) as eg:
+            getattr(gpu, half)(f, 0.0, 1e-4, make_field(g, 0.0))
+        assert eg.value.cause is TableRangeError
+        assert eg.value.line == eo.value.line
