@@ -3,7 +3,9 @@
 HBM roofline (BASELINE.json metric) on configs[3] -- the large grid
 Nr=8192 x Nz=16384, fixed dt 1e-5 -- one JSON line on rank 0.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--mode fast|exact]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--mode exact|fast]
+
+The default mode is exact: bit-identical to the reference AdiStepper.
   python bench.py --impl reference   # the reference's own CPU AdiStepper
 
 A "step" is one accepted ADI time step (AdiStepper::step, solver.cpp:356-373)
@@ -129,7 +131,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default=os.environ.get("PCGPU_BENCH_MODE", "fast"),
+    ap.add_argument("--mode", default=os.environ.get("PCGPU_BENCH_MODE", "exact"),
                     choices=["exact", "fast"])
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--cpu-nz", type=int, default=512, help="z-slice of the CPU sample")
@@ -238,6 +240,8 @@ def main():
         host_pinned = torch.from_numpy(np.ascontiguousarray(host.T)).pin_memory()
         hp = host_pinned.numpy().T  # (nr, nz) F-ordered view of pinned memory
         n_e2e = max(1, min(args.steps, 3))
+        r = stepper.step(hp, t_end)  # untimed: allocates the host-path staging buffer
+        t_end += r.tau_used
         upd = 0.0
         if pg:
             pg.barrier()
@@ -270,7 +274,10 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": dict(grid_desc, mode=args.mode, parallelism=f"replicas x{world}",
+            "config": dict(grid_desc, mode=args.mode, kernels=stepper.describe(),
+                           parity="bit-identical to the reference" if args.mode == "exact"
+                           else "reference rounding-noise floor",
+                           parallelism=f"replicas x{world}",
                            l2="inputs > L2 (1 GiB FP64 fields)",
                            picard={"radial_iters": stats["radial_iterations"],
                                    "axial_iters": stats["axial_iterations"],
