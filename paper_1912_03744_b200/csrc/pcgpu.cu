@@ -496,6 +496,7 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
           P.mats[m].uniform[p] = 2;
           P.mats[m].inv_h[p] = 0.0;
           P.mats[m].xmode[p] = 2;
+          P.mats[m].rdt[p] = 1.0 / (t.t[1] - t.t[0]);  // RN(1/(t1 - t0)) for div_rn
         } else if (t.n >= 3) {
           // Uniform-knot bracket guess (exactness is kept by the device fix-up).
           const double inv_h = (t.n - 1) / (t.t[t.n - 1] - t.t[0]);
