@@ -563,6 +563,42 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
       if (P.mats[m].n[2] > 0 && P.mats[m].xmode[2] != 2) P.exact_x = 0;
     }
     if (std::getenv("PCGPU_NO_EXACTX")) P.exact_x = 0;
+    // exact lean: exact_x and one knot grid per property (cv, lambda) across
+    // layers -- per-property lookup constants, guard pairs for the clamps
+    P.exact_lean = P.exact_x && d->n_layers <= kMaxLayers;
+    for (int p = 0; p < 2 && P.exact_lean; ++p) {
+      const DevMaterial& a = P.mats[0];
+      for (int m = 1; m < d->n_layers; ++m) {
+        const DevMaterial& b = P.mats[m];
+        if (a.n[p] != b.n[p] || a.t_first[p] != b.t_first[p] || a.t_last[p] != b.t_last[p] ||
+            a.inv_h[p] != b.inv_h[p])
+          P.exact_lean = 0;
+      }
+    }
+    if (std::getenv("PCGPU_NO_EXACTLEAN")) P.exact_lean = 0;
+    std::vector<double> xe;
+    if (P.exact_lean) {
+      for (int p = 0; p < 2; ++p) {
+        const int n = P.mats[0].n[p];
+        P.xe_t0[p] = P.mats[0].t_first[p];
+        P.xe_tK[p] = P.mats[0].t_last[p];
+        P.xe_inv_h[p] = P.mats[0].inv_h[p];
+        P.xe_n[p] = n;
+        P.xe_base[p] = static_cast<int>(xe.size() / 2);
+        for (int m = 0; m < d->n_layers; ++m) {
+          const pcgpu_table& t = p == 0 ? d->materials[m].cv : d->materials[m].lambda;
+          xe.push_back(t.v[0]);
+          xe.push_back(0.0);
+          for (int k = 1; k < n; ++k) {
+            xe.push_back(t.v[k - 1]);
+            xe.push_back(t.v[k] - t.v[k - 1]);
+          }
+          xe.push_back(t.v[n - 1]);
+          xe.push_back(0.0);
+        }
+      }
+      for (int m = 0; m < d->n_layers; ++m) P.xe_rho[m] = P.mats[m].rho;
+    }
     P.exact_ws = std::getenv("PCGPU_NO_EXACTWS") ? 0 : 1;
     std::vector<double> lt, lab;  // lean tables, uploaded below
     if (P.lean) {
@@ -649,6 +685,7 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
     }
     P.ivl = up(ivl);
     P.xpair = up(xpair);
+    if (P.exact_lean) P.xe_tab = up(xe);
     P.source_kind = d->source_kind;
     P.source_layer = d->source_layer;
     P.amplitude = d->amplitude;
@@ -756,7 +793,7 @@ int32_t pcgpu_describe(const pcgpu_stepper* h, char* buf, int32_t len) {
     s = "mode=exact lines=";
     s += h->P.exact_ws ? "ws" : "thread";
     s += " lookups=";
-    s += h->P.exact_x ? "exact-x" : "generic";
+    s += h->P.exact_lean ? "exact-lean" : (h->P.exact_x ? "exact-x" : "generic");
   } else {
     s = "mode=fast lookups=";
     s += h->P.lean ? "lean" : (h->P.all_u2 ? "u2" : "generic");

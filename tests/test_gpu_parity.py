@@ -474,12 +474,21 @@ def _cfg4s():
 
 def test_exact_selects_ws_and_exact_x_for_configs(cuda):
     gpu = gpu_stepper(_cfg4s(), "exact")
-    assert gpu.describe() == "mode=exact lines=ws lookups=exact-x"
+    assert gpu.describe() == "mode=exact lines=ws lookups=exact-lean"
     gpu = gpu_stepper(configs.step_cell(True), "exact")
     assert gpu.describe().startswith("mode=exact lines=ws")
 
 
-def test_exact_x_out_of_range_clamp_events_bitwise(cuda):
+@pytest.fixture(params=["exact-lean", "exact-x"])
+def lookup_kind(request, monkeypatch):
+    """Both exact lookup variants the BASELINE configs can select (exact-x is
+    what tables with per-layer knot grids get)."""
+    if request.param == "exact-x":
+        monkeypatch.setenv("PCGPU_NO_EXACTLEAN", "1")
+    return request.param
+
+
+def test_exact_x_out_of_range_clamp_events_bitwise(cuda, lookup_kind):
     """Cells below the power-law tables (4..300 K) in every layer: clamp events
     are counted per layer exactly as the reference counts them, and the fields
     stay bit-identical. (A hot spot above 300 K in a 4.2 K cell makes the
@@ -492,6 +501,7 @@ def test_exact_x_out_of_range_clamp_events_bitwise(cuda):
     f[50:52, 5:7] = 3.95
     f[63, 40] = 3.97
     port, gpu = PortStepper(case), gpu_stepper(case, "exact")
+    assert gpu.describe().endswith("lookups=" + lookup_kind)
     fo = f.copy(order="F")
     te_o, _, res_o = port.run(fo, 0.0, 6)
     fg = to_dev(f)
@@ -505,7 +515,7 @@ def test_exact_x_out_of_range_clamp_events_bitwise(cuda):
     assert sum(1 for c in port.clamp_events() if c) >= 2
 
 
-def test_exact_x_strict_range_lowest_line(cuda):
+def test_exact_x_strict_range_lowest_line(cuda, lookup_kind):
     case = _cfg4s()
     case.solver.range_policy = RangePolicy.Strict
     g = case.grid()
