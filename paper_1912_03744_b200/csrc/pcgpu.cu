@@ -576,6 +576,18 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
       }
     }
     if (std::getenv("PCGPU_NO_EXACTLEAN")) P.exact_lean = 0;
+    // div_rn precondition: every per-row / per-table denominator it divides by
+    // has |b| in [2^-100, 2^100]
+    {
+      auto in = [](double b) { b = std::fabs(b); return b >= 0x1p-100 && b <= 0x1p100; };
+      P.div_ok = 1;
+      for (int j = 0; j < nz; ++j)
+        if (!in(d->gap_z[j]) || !in(0.5 * (d->gap_z[j] + d->gap_z[j + 1]))) P.div_ok = 0;
+      if (!in(d->gap_z[nz])) P.div_ok = 0;
+      for (int m = 0; m < d->n_layers; ++m)
+        if (P.mats[m].xmode[2] == 2 && !in(P.mats[m].t_last[2] - P.mats[m].t_first[2]))
+          P.div_ok = 0;
+    }
     std::vector<double> xe;
     if (P.exact_lean) {
       for (int p = 0; p < 2; ++p) {

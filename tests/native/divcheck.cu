@@ -34,7 +34,7 @@ __global__ void check(unsigned long long seed, long long n, int emax_a, int emax
     const double a = rnd(h1, emax_a);
     const double b = rnd(h2, emax_b);
     const double rb = __drcp_rn(b);
-    const double q = div_rn(a, b, rb);
+    const double q = div_rn(a, b, rb, true);
     const double r = a / b;
     if (__double_as_longlong(q) != __double_as_longlong(r)) {
       if (atomicAdd(bad, 1ull) == 0) {
@@ -46,15 +46,18 @@ __global__ void check(unsigned long long seed, long long n, int emax_a, int emax
 }
 
 __global__ void specials(unsigned long long* bad) {
-  const double v[] = {0.0, -0.0, 1.0, -1.0, 3.0, 1e-310, -1e-310, 1e308, -1e308,
-                      __longlong_as_double(0x7ff0000000000000ll),
-                      __longlong_as_double(static_cast<long long>(0xfff0000000000000ull)),
-                      __longlong_as_double(0x7ff8000000000000ll), 0x1p-1022, 0x1p1023,
-                      0x1p-900, 0x1p900, 7.0, 1.0 / 3.0};
-  const int n = sizeof(v) / sizeof(v[0]);
-  for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
-    const double a = v[i / n], b = v[i % n];
-    const double q = div_rn(a, b, __drcp_rn(b)), r = a / b;
+  // a: anything; b: the precondition's range [2^-100, 2^100] (both signs)
+  const double va[] = {0.0, -0.0, 1.0, -1.0, 3.0, 1e-310, -1e-310, 1e308, -1e308,
+                       __longlong_as_double(0x7ff0000000000000ll),
+                       __longlong_as_double(static_cast<long long>(0xfff0000000000000ull)),
+                       __longlong_as_double(0x7ff8000000000000ll), 0x1p-1022, 0x1p1023,
+                       0x1p-800, 0x1p800, -0x1p-800, 0x1.fffffffffffffp-801, 7.0, 1.0 / 3.0};
+  const double vb[] = {1.0, -1.0, 3.0, 0x1p-100, -0x1p-100, 0x1p100, 0x1.fffffffffffffp99,
+                       7.0, 1.0 / 3.0, 1e-7, 1e3};
+  const int na = sizeof(va) / sizeof(va[0]), nb = sizeof(vb) / sizeof(vb[0]);
+  for (int i = threadIdx.x; i < na * nb; i += blockDim.x) {
+    const double a = va[i / nb], b = vb[i % nb];
+    const double q = div_rn(a, b, __drcp_rn(b), true), r = a / b;
     const bool both_nan = q != q && r != r;
     if (!both_nan && __double_as_longlong(q) != __double_as_longlong(r)) atomicAdd(bad, 1ull);
   }
@@ -67,8 +70,9 @@ int main(int argc, char** argv) {
   cudaMalloc(&bad, 8);
   cudaMalloc(&ex, 16);
   cudaMemset(bad, 0, 8);
-  // physical ranges (what the kernels divide) and wide ranges
-  const int ranges[][2] = {{40, 40}, {200, 200}, {1000, 1000}, {20, 8}};
+  // exponent ranges (a, b): physical values, and a up to the double range with
+  // b within the precondition's [2^-100, 2^100]
+  const int ranges[][2] = {{40, 40}, {200, 100}, {1000, 100}, {20, 8}};
   unsigned long long total_bad = 0, h;
   for (int r = 0; r < 4; ++r) {
     check<<<148 * 16, 256>>>(0x1234567ull + r, n / 4, ranges[r][0], ranges[r][1], bad, ex);
