@@ -308,7 +308,7 @@ def run_partitioned(args, case, rank, world, local, pg, grid_desc, metric):
     dev = torch.device(f"cuda:{local}")
     uid = share_unique_id(rank, dev)
     part = PartitionedAdi(g, case.materials, make_source(case, g), case.timing, case.solver,
-                          device=local, rank=rank, world=world, unique_id=uid)
+                          device=local, rank=rank, world=world, unique_id=uid, mode=args.mode)
     field = torch.full((g.nz(), g.nr()), case.solver.T0, dtype=torch.float64, device=dev).t()
     part.set_field(field)
     t, _, _ = part.run(0.0, args.warmup)
@@ -344,15 +344,16 @@ def run_partitioned(args, case, rank, world, local, pg, grid_desc, metric):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": dict(grid_desc, mode="fast", parallelism=f"z-slab/r-slab x{world}",
+            "config": dict(grid_desc, mode=args.mode, parallelism=f"z-slab/r-slab x{world}",
                            l2="inputs > L2", rank0_slabs={"z": [z0, z1], "r": [r0, r1]},
                            picard={"radial_iters": stats["radial_iterations"],
                                    "axial_iters": stats["axial_iterations"],
                                    "halvings": stats["halvings"]}),
             "transpose": {"ms_per_transpose_max_rank": float(tr.item()),
-                          "transposes_per_step": 2, "fields_per_transpose": 2,
-                          "bytes_per_rank_per_transpose":
-                              2 * 8 * g.nr() * g.nz() // world * (world - 1) // world},
+                          "transposes_per_step": 3 if args.mode == "exact" else 2,
+                          "fields_per_step": 4,
+                          "bytes_per_rank_per_step":
+                              4 * 8 * g.nr() * g.nz() // world * (world - 1) // world},
             "clocks": clk.summary(), "gpu_launches": launches, "e2e": None,
         }
         print(json.dumps(line))

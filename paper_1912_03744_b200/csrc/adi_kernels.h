@@ -34,6 +34,27 @@ void launch_axial_exact(const DevProblem& P, int it, double eps, const double* T
                         const double* ThN, const double* kbarN, const double* explN,
                         double* outN, double* wN, double* xN, DevStatus* st, cudaStream_t s);
 
+// ---- partitioned (multi-GPU) slabs, exact mode (adi_exact.cu) ----
+// z-slab: radial lines j0..j0+nj-1, T layout [i][j-j0] (ld nj);
+// r-slab: axial lines i0..i0+ni-1, N layout [j][i-i0] (ld ni).
+void launch_radial_exact_slab(const DevProblem& P, int it, double eps, double half_k,
+                              double pulse, int j0, int nj, const double* TsT, const double* TcT,
+                              const double* explT, const double* powT, double* outT, double* wT,
+                              double* xT, DevStatus* st, cudaStream_t s);
+void launch_axial_exact_slab(const DevProblem& P, int it, double eps, int i0, int ni,
+                             const double* TsN, const double* ThN, const double* kbarN,
+                             const double* explN, double* outN, double* wN, double* xN,
+                             DevStatus* st, cudaStream_t s);
+// K3 on an r-slab: explR = Lambda_z[TR]
+void launch_expl_rslab_exact(const DevProblem& P, int i0, int ni, const double* TR,
+                             double* explR, DevStatus* st, cudaStream_t s);
+// K4 without K-bar on a z-slab: explZ = Lambda_r[halfZ] + X(halfZ)
+void launch_rhs_zslab_exact(const DevProblem& P, double pulse, int j0, int nj,
+                            const double* halfZ, double* explZ, DevStatus* st, cudaStream_t s);
+// K-bar on an r-slab
+void launch_kbar_rslab_exact(const DevProblem& P, double half_k, int i0, int ni,
+                             const double* halfR, double* kbarR, DevStatus* st, cudaStream_t s);
+
 // ---- layout helpers (masked: only in-mask cells are written) ----
 void launch_transpose_N2T(const DevProblem& P, const double* srcN, double* dstT, cudaStream_t s);
 void launch_transpose_T2N(const DevProblem& P, const double* srcT, double* dstN, cudaStream_t s);

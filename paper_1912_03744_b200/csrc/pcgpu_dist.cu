@@ -176,6 +176,11 @@ struct RankState {
   double *zTc = nullptr, *zExpl = nullptr, *zHalf = nullptr, *zIter = nullptr, *zR = nullptr;
   double *rHalf = nullptr, *rExpl = nullptr, *rOut = nullptr, *rIter = nullptr;
   double *send = nullptr, *recv = nullptr;
+  // exact mode: Thomas scratch on both slabs, K-bar and the r-slab copy of
+  // the step's anchor (Lambda_z is recomputed from it every attempt, like the
+  // single-GPU stepper)
+  double *zW = nullptr, *zX = nullptr, *rW = nullptr, *rX = nullptr;
+  double *rKbar = nullptr, *rTc = nullptr;
   DevStatus* st = nullptr;
 };
 
@@ -221,6 +226,7 @@ struct pcgpu_dist {
     return p;
   }
 
+  bool exact() const { return d.mode == PCGPU_MODE_EXACT; }
   int zcount(int p) const { return zb[p + 1] - zb[p]; }
   int rcount(int p) const { return rb[p + 1] - rb[p]; }
 
@@ -331,10 +337,173 @@ struct pcgpu_dist {
     }
   }
 
-  void reset_status() {
+  void reset_status(bool clear_err = true) {
     for (RankState& R : ranks) {
       DCK(cudaMemsetAsync(R.st->delta, 0, sizeof(R.st->delta), stream));
-      DCK(cudaMemsetAsync(&R.st->err, 0xff, sizeof(R.st->err), stream));
+      if (clear_err) DCK(cudaMemsetAsync(&R.st->err, 0xff, sizeof(R.st->err), stream));
+    }
+  }
+
+  // Exact-mode all-to-all of k fields between the dense slabs.
+  // z2r: z-slab T layout [i][j - j0] (ld nj) -> r-slab N layout [j][i - i0] (ld ni);
+  // r2z: the reverse. The block a rank sends to q is a contiguous row range of
+  // its slab (rows i in R_q, resp. j in Z_q), so it is sent straight from the
+  // field; the receiver transposes each block into place.
+  void transpose_exact(bool z2r, int k, double* const* const* src, double* const* const* dst) {
+    if (timing) DCK(cudaEventRecord(ev0, stream));
+    // exchange into recv staging: per field f, blocks ordered by source rank
+    auto blk_rows = [&](int q) { return z2r ? rcount(q) : zcount(q); };  // rows sent to q
+    auto src_cols = [&](int p) { return z2r ? zcount(p) : rcount(p); };  // ld of p's slab
+    auto row0 = [&](int q) { return z2r ? rb[q] : zb[q]; };
+    if (local) {
+      for (int f = 0; f < k; ++f)
+        for (int q = 0; q < nranks; ++q) {
+          size_t roff = static_cast<size_t>(f) * (z2r ? static_cast<size_t>(rcount(q)) * d.nz
+                                                      : static_cast<size_t>(zcount(q)) * d.nr);
+          for (int p = 0; p < nranks; ++p) {
+            const size_t n = static_cast<size_t>(blk_rows(q)) * src_cols(p);
+            if (n)
+              DCK(cudaMemcpyAsync(ranks[q].recv + roff,
+                                  src[f][p] + static_cast<size_t>(row0(q)) * src_cols(p),
+                                  sizeof(double) * n, cudaMemcpyDeviceToDevice, stream));
+            roff += n;
+          }
+        }
+    } else {
+      RankState& R = ranks[0];
+      const int me = R.rank;
+      NCK(g_nccl.groupStart());
+      for (int f = 0; f < k; ++f) {
+        size_t roff = static_cast<size_t>(f) * (z2r ? static_cast<size_t>(R.ni) * d.nz
+                                                    : static_cast<size_t>(R.nj) * d.nr);
+        for (int q = 0; q < nranks; ++q) {
+          const size_t sn = static_cast<size_t>(blk_rows(q)) * src_cols(me);
+          const size_t rn = static_cast<size_t>(blk_rows(me)) * src_cols(q);
+          if (sn)
+            NCK(g_nccl.send(src[f][0] + static_cast<size_t>(row0(q)) * src_cols(me), sn,
+                            ncclDouble, q, comm, stream));
+          if (rn) NCK(g_nccl.recv(R.recv + roff, rn, ncclDouble, q, comm, stream));
+          roff += rn;
+        }
+      }
+      NCK(g_nccl.groupEnd());
+    }
+    // unpack: block from p is [rows of mine][cols of p] -> transpose into place
+    for (size_t lr = 0; lr < ranks.size(); ++lr) {
+      RankState& R = ranks[lr];
+      const int me = R.rank;
+      for (int f = 0; f < k; ++f) {
+        size_t off = static_cast<size_t>(f) * (z2r ? static_cast<size_t>(R.ni) * d.nz
+                                                   : static_cast<size_t>(R.nj) * d.nr);
+        for (int p = 0; p < nranks; ++p) {
+          const int rows = blk_rows(me), cols = src_cols(p);
+          // z2r: block [i - i0][j - zb[p]] -> dst[j * ni + (i - i0)], j = zb[p] + c
+          // r2z: block [j - j0][i - rb[p]] -> dst[i * nj + (j - j0)], i = rb[p] + c
+          const int c0 = z2r ? zb[p] : rb[p];
+          const long long dld = z2r ? R.ni : R.nj;
+          transpose_block(R.recv + off, cols, rows, cols, dst[f][lr] + c0 * dld, dld, stream);
+          off += static_cast<size_t>(rows) * cols;
+        }
+      }
+    }
+    ++transposes;
+    if (timing) {
+      DCK(cudaEventRecord(ev1, stream));
+      DCK(cudaEventSynchronize(ev1));
+      float ms = 0;
+      DCK(cudaEventElapsedTime(&ms, ev0, ev1));
+      transpose_ms += ms;
+    }
+  }
+
+  // One exact ADI step (solver.cpp:356-373) on the partitioned state: z-slab
+  // anchor zTc (T layout) and its r-slab copy rTc (N layout).
+  int step_exact(double t, pcgpu_step_result* r, double* updates) {
+    double tau = pcgpu_host_initial_tau(d, t);
+    *r = pcgpu_step_result{};
+    const size_t nl = ranks.size();
+    std::vector<double*> a(nl), b(nl), c(nl), e(nl);
+    for (;;) {
+      const double pulse = d.source_kind == PCGPU_SOURCE_JOULE
+                               ? pcgpu_host_pulse_value(d, t + 0.5 * tau) : 0.0;
+      const double hk = 2.0 / tau;
+      // ---- radial half-step: Lambda_z[T_cur] on the r-slabs -> z-slabs ----
+      reset_status();
+      for (size_t lr = 0; lr < nl; ++lr) {
+        RankState& R = ranks[lr];
+        launch_expl_rslab_exact(P, R.i0, R.ni, R.rTc, R.rExpl, R.st, stream);
+        a[lr] = R.rExpl;
+        b[lr] = R.zExpl;
+      }
+      {
+        double* const* s1[1] = {a.data()};
+        double* const* d1[1] = {b.data()};
+        transpose_exact(false, 1, s1, d1);
+      }
+      auto zsrc = [&](RankState& R, int it) -> const double* {
+        return it == 1 ? R.zTc : (it % 2 == 0 ? R.zHalf : R.zIter);
+      };
+      auto zdst = [&](RankState& R, int it) -> double* { return it % 2 == 1 ? R.zHalf : R.zIter; };
+      int conv = picard(pred_r, [&](size_t lr, int it) {
+        RankState& R = ranks[lr];
+        launch_radial_exact_slab(P, it, d.epsilon, hk, pulse, R.j0, R.nj, zsrc(R, it), R.zTc,
+                                 R.zExpl, nullptr, zdst(R, it), R.zW, R.zX, R.st, stream);
+      }, &r->radial, true);
+      if (conv < 0) return -conv;
+      *updates += static_cast<double>(active) * r->radial.iterations;
+      if (conv > 0) {
+        // ---- axial half-step: Lambda_r + X on the z-slabs, -> r-slabs, K-bar ----
+        reset_status();
+        for (size_t lr = 0; lr < nl; ++lr) {
+          RankState& R = ranks[lr];
+          a[lr] = zdst(R, conv);
+          launch_rhs_zslab_exact(P, pulse, R.j0, R.nj, a[lr], R.zR, R.st, stream);
+          b[lr] = R.zR;
+          c[lr] = R.rHalf;
+          e[lr] = R.rExpl;
+        }
+        {
+          double* const* s2[2] = {a.data(), b.data()};
+          double* const* d2[2] = {c.data(), e.data()};
+          transpose_exact(true, 2, s2, d2);
+        }
+        for (RankState& R : ranks)
+          launch_kbar_rslab_exact(P, hk, R.i0, R.ni, R.rHalf, R.rKbar, R.st, stream);
+        reset_status(false);  // keep errors of the K4 passes
+        auto rsrc = [&](RankState& R, int it) -> const double* {
+          return it == 1 ? R.rHalf : (it % 2 == 0 ? R.rOut : R.rIter);
+        };
+        auto rdst = [&](RankState& R, int it) -> double* { return it % 2 == 1 ? R.rOut : R.rIter; };
+        const int aconv = picard(pred_a, [&](size_t lr, int it) {
+          RankState& R = ranks[lr];
+          launch_axial_exact_slab(P, it, d.epsilon, R.i0, R.ni, rsrc(R, it), R.rHalf, R.rKbar,
+                                  R.rExpl, rdst(R, it), R.rW, R.rX, R.st, stream);
+        }, &r->axial, false);
+        if (aconv < 0) return -aconv;
+        *updates += static_cast<double>(active) * r->axial.iterations;
+        if (aconv > 0) {
+          // accept: the r-slab result becomes the anchor; -> z-slabs
+          for (size_t lr = 0; lr < nl; ++lr) {
+            RankState& R = ranks[lr];
+            double* res = rdst(R, aconv);
+            if (res == R.rOut) std::swap(R.rOut, R.rTc); else std::swap(R.rIter, R.rTc);
+            a[lr] = R.rTc;
+            b[lr] = R.zTc;
+          }
+          double* const* s1[1] = {a.data()};
+          double* const* d1[1] = {b.data()};
+          transpose_exact(false, 1, s1, d1);
+          r->tau_used = tau;
+          return PCGPU_OK;
+        }
+      }
+      tau *= 0.5;
+      ++r->halvings;
+      if (tau < tau_floor) {
+        err = "time step fell below floor";
+        return PCGPU_ERR_TAU_FLOOR;
+      }
+      r->axial = pcgpu_outcome{};
     }
   }
 
@@ -403,6 +572,10 @@ struct pcgpu_dist {
   // One ADI step (solver.cpp:356-373) on the partitioned state
   // (z-slab anchor zTc + zExpl = Lambda_z[zTc]).
   int step(double t, pcgpu_step_result* r, double* updates) {
+    return exact() ? step_exact(t, r, updates) : step_fast(t, r, updates);
+  }
+
+  int step_fast(double t, pcgpu_step_result* r, double* updates) {
     double tau = pcgpu_host_initial_tau(d, t);
     *r = pcgpu_step_result{};
     for (;;) {
@@ -491,8 +664,8 @@ int pcgpu_dist_create(const pcgpu_desc* d, int32_t rank, int32_t nranks, const v
   if (!d || !out || nranks < 1) return PCGPU_ERR_ARG;
   *out = nullptr;
   std::string v = pcgpu_validate_desc(d);
-  if (v.empty() && d->mode != PCGPU_MODE_FAST)
-    v = "pcgpu_dist: the partitioned stepper runs the fast-mode kernels";
+  if (v.empty() && d->mode == PCGPU_MODE_EXACT && d->source_kind == PCGPU_SOURCE_FIELD)
+    v = "pcgpu_dist: exact mode supports Null and Joule sources";
   if (!v.empty()) {
     g_dist_create_error = v;
     return PCGPU_ERR_CONFIG;
@@ -543,8 +716,18 @@ int pcgpu_dist_create(const pcgpu_desc* d, int32_t rank, int32_t nranks, const v
       R.rOut = h->alloc(rc);
       R.rIter = h->alloc(rc);
       // staging: z->r sends 2*zc, receives 2*rc; r->z the reverse
-      R.send = h->alloc(2 * std::max(zc, rc));
-      R.recv = h->alloc(2 * std::max(zc, rc));
+      if (d->mode == PCGPU_MODE_EXACT) {
+        R.zW = h->alloc(zc);
+        R.zX = h->alloc(zc);
+        R.rW = h->alloc(rc);
+        R.rX = h->alloc(rc);
+        R.rKbar = h->alloc(rc);
+        R.rTc = h->alloc(rc);
+        R.recv = h->alloc(2 * std::max(zc, rc));  // sends go straight from the fields
+      } else {
+        R.send = h->alloc(2 * std::max(zc, rc));
+        R.recv = h->alloc(2 * std::max(zc, rc));
+      }
       DevStatus* st = nullptr;
       DCK(cudaMalloc(&st, sizeof(DevStatus)));
       h->allocs.push_back(st);
@@ -585,6 +768,26 @@ int pcgpu_dist_slabs(const pcgpu_dist* h, int32_t* z0, int32_t* z1, int32_t* r0,
 // Every rank passes the full initial field (device, N layout). Each rank
 // keeps its z-slab lines and Lambda_z on them (computed on the full field).
 int pcgpu_dist_set_field(pcgpu_dist* h, const double* fieldN) {
+  if (h->exact()) {
+    try {
+      const int nr = h->d.nr;
+      for (RankState& R : h->ranks) {
+        // z-slab T layout [i][j - j0] <- N rows j0 .. j0+nj-1
+        transpose_block(fieldN + static_cast<size_t>(R.j0) * nr, nr, R.nj, nr, R.zTc, R.nj,
+                        h->stream);
+        // r-slab N layout [j][i - i0] <- columns i0 .. i0+ni-1
+        if (R.ni)
+          DCK(cudaMemcpy2DAsync(R.rTc, sizeof(double) * R.ni, fieldN + R.i0,
+                                sizeof(double) * nr, sizeof(double) * R.ni, h->d.nz,
+                                cudaMemcpyDeviceToDevice, h->stream));
+      }
+      DCK(cudaStreamSynchronize(h->stream));
+    } catch (const DistError& e) {
+      h->err = e.what;
+      return e.code;
+    }
+    return PCGPU_OK;
+  }
   try {
     const int nr = h->d.nr, nz = h->d.nz;
     const size_t cells = static_cast<size_t>(nr) * nz;
@@ -614,10 +817,15 @@ int pcgpu_dist_set_field(pcgpu_dist* h, const double* fieldN) {
 int pcgpu_dist_get_field(pcgpu_dist* h, double* fieldN) {
   try {
     const int nr = h->d.nr;
-    for (RankState& R : h->ranks)
-      DCK(cudaMemcpyAsync(fieldN + static_cast<size_t>(R.j0) * nr, R.zTc,
-                          sizeof(double) * static_cast<size_t>(R.nj) * nr,
-                          cudaMemcpyDeviceToDevice, h->stream));
+    for (RankState& R : h->ranks) {
+      if (h->exact())  // z-slab T layout -> N rows j0 .. j0+nj-1
+        transpose_block(R.zTc, R.nj, nr, R.nj, fieldN + static_cast<size_t>(R.j0) * nr, nr,
+                        h->stream);
+      else
+        DCK(cudaMemcpyAsync(fieldN + static_cast<size_t>(R.j0) * nr, R.zTc,
+                            sizeof(double) * static_cast<size_t>(R.nj) * nr,
+                            cudaMemcpyDeviceToDevice, h->stream));
+    }
     DCK(cudaStreamSynchronize(h->stream));
   } catch (const DistError& e) {
     h->err = e.what;

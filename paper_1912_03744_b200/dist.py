@@ -7,7 +7,8 @@ runs the z-slab radial sweep, the all-to-all transposes and the per-iteration
 allreduce(max) of the Picard norm itself (NCCL on the library's stream).
 With ``emulate=P`` the library runs P virtual ranks in this process on one
 GPU -- the same code path minus NCCL -- which is how the partitioned path is
-validated on a single GPU (bit-identical to the single-GPU fast path).
+validated on a single GPU (bit-identical to the single-GPU stepper of the
+same mode).
 """
 from __future__ import annotations
 
@@ -56,16 +57,25 @@ def share_unique_id(rank: int, device=None) -> bytes:
 
 
 class PartitionedAdi:
-    """z-slab / r-slab partitioned AdiStepper (fast-mode kernels)."""
+    """z-slab / r-slab partitioned AdiStepper.
+
+    mode "exact": the exact kernels on dense slabs -- bit-identical to the
+    single-GPU exact stepper (and so to the reference); mode "fast": the
+    partitioned fast-mode line solver."""
 
     def __init__(self, grid, mats, source, timing, cfg, device: int = 0,
                  rank: int = 0, world: int = 1, emulate: Optional[int] = None,
-                 unique_id: Optional[bytes] = None):
+                 unique_id: Optional[bytes] = None, mode: str = "exact"):
         self._lib = N.load()
         cfg.validate()
         timing.validate()
         self._grid = grid
-        self._desc, self._keep = build_desc(grid, mats, source, timing, cfg, N.MODE_FAST, device)
+        if mode not in ("exact", "fast"):
+            raise ValueError("mode must be 'exact' or 'fast'")
+        self.mode = mode
+        self._desc, self._keep = build_desc(grid, mats, source, timing, cfg,
+                                            N.MODE_EXACT if mode == "exact" else N.MODE_FAST,
+                                            device)
         h = C.c_void_p()
         if emulate is not None:
             rc = self._lib.pcgpu_dist_create(C.byref(self._desc), 0, int(emulate), None,

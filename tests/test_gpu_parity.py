@@ -411,7 +411,60 @@ def test_fast_vs_exact_cfg3_full_size(cuda):
 
 # ---------------------------------------------------------------------------
 # Partitioned (multi-GPU) stepper, P ranks emulated in-process on one GPU:
-# bit-identical to the single-GPU fast path.
+# bit-identical to the single-GPU stepper of the same mode; in
+# exact mode that is the reference itself.
+@pytest.mark.parametrize("name,nranks,steps", [
+    ("cfg0", 2, 30), ("cfg0", 3, 30), ("cfg4s", 4, 6), ("cfg4s", 8, 6), ("cfg4s", 1, 4),
+])
+def test_partitioned_exact_emulated_bitwise(cuda, name, nranks, steps):
+    from paper_1912_03744_b200.dist import PartitionedAdi
+    case = configs.cfg0() if name == "cfg0" else \
+        configs.scaled(configs.cfg4(), [706, 71, 212, 35], 2048, 1400)
+    g = case.grid()
+    src = configs.make_source(case, g)
+    single = gpu_stepper(case, "exact")
+    f1 = to_dev(make_field(g, case.solver.T0))
+    _, _, r1 = single.run(f1, 0.0, steps, keep_results=True)
+    part = PartitionedAdi(g, case.materials, src, case.timing, case.solver, device=0,
+                          emulate=nranks, mode="exact")
+    f0 = to_dev(make_field(g, case.solver.T0))
+    part.set_field(f0)
+    part.enable_timing(True)
+    _, _, r2 = part.run(0.0, steps, keep_results=True)
+    out = to_dev(make_field(g, 0.0))
+    part.get_field(out)
+    assert _seq(r1).tolist() == _seq(r2).tolist()
+    m = g.mask()
+    assert np.array_equal(to_host(out)[m], to_host(f1)[m])
+    tm = part.timing()
+    assert tm["transposes"] == 3 * steps and tm["allreduces"] > 0
+
+
+def test_partitioned_exact_halving_and_clamps_vs_oracle(cuda):
+    """Partitioned exact run with tau halvings and clamp events, against the
+    oracle (the reference's algorithm) directly."""
+    from paper_1912_03744_b200.dist import PartitionedAdi
+    case = _cfg4s()
+    g = case.grid()
+    f = make_field(g, case.solver.T0)
+    f[10:12, 20:23] = 3.9
+    f[46, 30:32] = 3.95
+    f[50:52, 5:7] = 3.95
+    port = PortStepper(case)
+    fo = f.copy(order="F")
+    _, _, res_o = port.run(fo, 0.0, 6)
+    assert sum(r.halvings for r in res_o) > 0
+    part = PartitionedAdi(g, case.materials, configs.make_source(case, g), case.timing,
+                          case.solver, device=0, emulate=3, mode="exact")
+    part.set_field(to_dev(f))
+    _, _, res_p = part.run(0.0, 6, keep_results=True)
+    out = to_dev(make_field(g, 0.0))
+    part.get_field(out)
+    assert np.array_equal(_seq(res_p), _seq(res_o))
+    m = g.mask()
+    assert np.array_equal(to_host(out)[m], fo[m])
+
+
 @pytest.mark.parametrize("name,nranks,steps", [
     ("cfg0", 2, 30), ("cfg0", 3, 30), ("cfg4s", 4, 6), ("cfg4s", 8, 6), ("cfg4s", 1, 4),
 ])
@@ -426,7 +479,7 @@ def test_partitioned_emulated_bitwise(cuda, name, nranks, steps):
     f1 = to_dev(make_field(g, case.solver.T0))
     _, _, r1 = single.run(f1, 0.0, steps, keep_results=True)
     part = PartitionedAdi(g, case.materials, src, case.timing, case.solver, device=0,
-                          emulate=nranks)
+                          emulate=nranks, mode="fast")
     f0 = to_dev(make_field(g, case.solver.T0))
     part.set_field(f0)
     part.enable_timing(True)
