@@ -309,6 +309,8 @@ def run_partitioned(args, case, rank, world, local, pg, grid_desc, metric):
     uid = share_unique_id(rank, dev)
     part = PartitionedAdi(g, case.materials, make_source(case, g), case.timing, case.solver,
                           device=local, rank=rank, world=world, unique_id=uid, mode=args.mode)
+    if args.mode == "exact" and os.environ.get("PCGPU_DIST_TRANSPORT", "peer") != "nccl":
+        part.enable_peer_transport()  # fused K3/K4 + peer stores over NVLink
     field = torch.full((g.nz(), g.nr()), case.solver.T0, dtype=torch.float64, device=dev).t()
     part.set_field(field)
     t, _, _ = part.run(0.0, args.warmup)
@@ -345,6 +347,7 @@ def run_partitioned(args, case, rank, world, local, pg, grid_desc, metric):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": dict(grid_desc, mode=args.mode, parallelism=f"z-slab/r-slab x{world}",
+                           transport=part.transport(),
                            l2="inputs > L2", rank0_slabs={"z": [z0, z1], "r": [r0, r1]},
                            picard={"radial_iters": stats["radial_iterations"],
                                    "axial_iters": stats["axial_iterations"],

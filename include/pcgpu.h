@@ -238,8 +238,8 @@ int32_t pcgpu_describe(const pcgpu_stepper* h, char* buf, int32_t len);
 /* ---- Partitioned stepper: one node of B200s ------------------
  * z-slabs (radial lines j) for the radial sweep, r-slabs (axial lines i) for
  * the axial sweep, all-to-all transposes between them, allreduce(max) of the
- * Picard norm every iteration. Fast-mode kernels; bit-identical to a
- * single-GPU fast-mode run. With nccl_id == NULL the library emulates
+ * Picard norm every iteration. Exact mode (bit-identical to the single-GPU
+ * exact stepper) or fast mode (bit-identical to a single-GPU fast run). With nccl_id == NULL the library emulates
  * `nranks` ranks in this process on desc->device (test/validation mode);
  * otherwise this process is rank `rank` of an NCCL communicator created from
  * the 128-byte id produced by pcgpu_nccl_unique_id on one rank and shared by
@@ -258,8 +258,21 @@ int pcgpu_dist_plan(const pcgpu_desc* desc, int32_t nranks, int32_t* zb, int32_t
 int pcgpu_dist_slabs(const pcgpu_dist* h, int32_t* z0, int32_t* z1, int32_t* r0, int32_t* r1);
 /* Every rank passes the full initial field (device, nr x nz column-major). */
 int pcgpu_dist_set_field(pcgpu_dist* h, const double* field_dev);
-/* Writes this process's z-slab lines into the full-size device field. */
+/* Writes this process's lines into the full-size device field: the r-slab
+ * columns (axial lines) in exact mode, the z-slab rows in fast mode. */
 int pcgpu_dist_get_field(pcgpu_dist* h, double* field_dev);
+/* Exact mode transport: 1 = peer stores from the fused slab passes (the
+ * default for emulated ranks; after pcgpu_dist_ipc_import for processes),
+ * 0 = NCCL all-to-all transposes. */
+int32_t pcgpu_dist_transport(const pcgpu_dist* h);
+/* Peer transport across processes (exact mode, one process per GPU): each
+ * rank exports PCGPU_DIST_IPC_BYTES of CUDA IPC handles for its slabs, the
+ * caller all-gathers them (rank order) and every rank imports the
+ * nranks * PCGPU_DIST_IPC_BYTES block; the fused K3/K4 passes then store into
+ * the peers' slabs over NVLink, ordered by an NCCL barrier. */
+#define PCGPU_DIST_IPC_BYTES 256
+int pcgpu_dist_ipc_export(pcgpu_dist* h, void* handles);
+int pcgpu_dist_ipc_import(pcgpu_dist* h, const void* all_handles);
 /* nsteps x step() with t += tau_used on the partitioned state. */
 int pcgpu_dist_run(pcgpu_dist* h, double t0, int32_t nsteps, pcgpu_step_result* results,
                    pcgpu_run_stats* stats);

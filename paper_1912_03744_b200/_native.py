@@ -14,6 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libpcgpu.so")
 
 PCGPU_ABI_VERSION = 1
+DIST_IPC_BYTES = 256
 
 # pcgpu_status
 OK, ERR_CONFIG, ERR_TAU_FLOOR, ERR_TABLE_RANGE, ERR_ZERO_PIVOT, ERR_CUDA, ERR_ARG = range(7)
@@ -79,7 +80,8 @@ EXPORTS = [
     "pcgpu_tridiag_batch", "pcgpu_nccl_unique_id", "pcgpu_dist_create", "pcgpu_dist_destroy",
     "pcgpu_dist_last_error", "pcgpu_dist_plan", "pcgpu_dist_slabs", "pcgpu_dist_set_field",
     "pcgpu_dist_get_field", "pcgpu_dist_run", "pcgpu_dist_stream", "pcgpu_dist_enable_timing",
-    "pcgpu_dist_timing", "pcgpu_dist_launch_count", "pcgpu_run_growth", "pcgpu_describe",
+    "pcgpu_dist_timing", "pcgpu_dist_launch_count", "pcgpu_run_growth", "pcgpu_describe", "pcgpu_dist_transport",
+    "pcgpu_dist_ipc_export", "pcgpu_dist_ipc_import",
 ]
 
 _lib = None
@@ -145,6 +147,9 @@ def load():
                                      C.POINTER(RunStats)]),
         "pcgpu_dist_stream": (vp, [vp]),
         "pcgpu_dist_launch_count": (C.c_int64, [vp]),
+        "pcgpu_dist_transport": (C.c_int32, [vp]),
+        "pcgpu_dist_ipc_export": (C.c_int, [vp, vp]),
+        "pcgpu_dist_ipc_import": (C.c_int, [vp, vp]),
         "pcgpu_dist_enable_timing": (C.c_int, [vp, C.c_int32]),
         "pcgpu_dist_timing": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                         C.POINTER(C.c_int64), C.POINTER(C.c_double),

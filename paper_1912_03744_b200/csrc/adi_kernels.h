@@ -55,6 +55,24 @@ void launch_rhs_zslab_exact(const DevProblem& P, double pulse, int j0, int nj,
 void launch_kbar_rslab_exact(const DevProblem& P, double half_k, int i0, int ni,
                              const double* halfR, double* kbarR, DevStatus* st, cudaStream_t s);
 
+// Fused compute + all-to-all (peer transport): destination slabs of every rank.
+constexpr int kMaxPeers = 16;
+struct PeerSlabs {
+  double* zTc[kMaxPeers];    // rank q's z-slab anchor, T layout [i][j - zb[q]]
+  double* zExpl[kMaxPeers];  // rank q's Lambda_z, same layout
+  double* rHalf[kMaxPeers];  // rank q's r-slab T_half, N layout [j][i - rb[q]]
+  double* rExpl[kMaxPeers];  // rank q's Lambda_r + X, same layout
+  int zb[kMaxPeers + 1], rb[kMaxPeers + 1];
+  int nranks;
+};
+// K3 on an r-slab, (Lambda_z, T_cur) stored into the owners' z-slabs
+void launch_expl_rslab_scatter(const DevProblem& P, int i0, int ni, const double* TR,
+                               const PeerSlabs& ps, DevStatus* st, cudaStream_t s);
+// K4 without K-bar on a z-slab, (T_half, Lambda_r + X) stored into the owners' r-slabs
+void launch_rhs_zslab_scatter(const DevProblem& P, double pulse, int j0, int nj,
+                              const double* halfZ, const PeerSlabs& ps, DevStatus* st,
+                              cudaStream_t s);
+
 // ---- layout helpers (masked: only in-mask cells are written) ----
 void launch_transpose_N2T(const DevProblem& P, const double* srcN, double* dstT, cudaStream_t s);
 void launch_transpose_T2N(const DevProblem& P, const double* srcT, double* dstN, cudaStream_t s);

@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -201,6 +202,13 @@ struct pcgpu_dist {
   std::string err;
   int64_t err_line = -1;
   int pred_r = 1, pred_a = 1;
+  // exact mode transport: peer stores from the fused slab passes (emulated
+  // ranks, or IPC-mapped peer slabs after pcgpu_dist_ipc_import), else NCCL
+  // all-to-all transposes
+  bool peer = false;
+  PeerSlabs ps{};
+  std::vector<void*> ipc_opened;
+  unsigned long long* d_barrier = nullptr;
   // timing
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double transpose_ms = 0;
@@ -211,6 +219,7 @@ struct pcgpu_dist {
 
   ~pcgpu_dist() {
     if (stream) cudaStreamSynchronize(stream);
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (comm && g_nccl.commDestroy) g_nccl.commDestroy(comm);
     for (void* p : allocs) cudaFree(p);
     if (st_host) cudaFreeHost(st_host);
@@ -231,6 +240,29 @@ struct pcgpu_dist {
   int rcount(int p) const { return rb[p + 1] - rb[p]; }
 
   // ---- collectives ----
+  // Cross-rank ordering point after peer stores (multi-process peer
+  // transport): every rank's scatter kernel has completed before any rank
+  // reads its slabs. Emulated ranks share one stream and need none.
+  void barrier() {
+    if (local) return;
+    NCK(g_nccl.allReduce(d_barrier, d_barrier, 1, ncclUint64, ncclMax, comm, stream));
+  }
+
+  void build_peer_table_local() {
+    ps = PeerSlabs{};
+    ps.nranks = nranks;
+    for (int q = 0; q <= nranks; ++q) {
+      ps.zb[q] = zb[q];
+      ps.rb[q] = rb[q];
+    }
+    for (RankState& R : ranks) {
+      ps.zTc[R.rank] = R.zTc;
+      ps.zExpl[R.rank] = R.zExpl;
+      ps.rHalf[R.rank] = R.rHalf;
+      ps.rExpl[R.rank] = R.rExpl;
+    }
+  }
+
   void allreduce_status(int it) {
     ++allreduces;
     if (local) {
@@ -429,13 +461,18 @@ struct pcgpu_dist {
       const double hk = 2.0 / tau;
       // ---- radial half-step: Lambda_z[T_cur] on the r-slabs -> z-slabs ----
       reset_status();
-      for (size_t lr = 0; lr < nl; ++lr) {
-        RankState& R = ranks[lr];
-        launch_expl_rslab_exact(P, R.i0, R.ni, R.rTc, R.rExpl, R.st, stream);
-        a[lr] = R.rExpl;
-        b[lr] = R.zExpl;
-      }
-      {
+      if (peer) {
+        // fused: Lambda_z and T_cur stored straight into the owners' z-slabs
+        for (RankState& R : ranks)
+          launch_expl_rslab_scatter(P, R.i0, R.ni, R.rTc, ps, R.st, stream);
+        barrier();
+      } else {
+        for (size_t lr = 0; lr < nl; ++lr) {
+          RankState& R = ranks[lr];
+          launch_expl_rslab_exact(P, R.i0, R.ni, R.rTc, R.rExpl, R.st, stream);
+          a[lr] = R.rExpl;
+          b[lr] = R.zExpl;
+        }
         double* const* s1[1] = {a.data()};
         double* const* d1[1] = {b.data()};
         transpose_exact(false, 1, s1, d1);
@@ -454,15 +491,20 @@ struct pcgpu_dist {
       if (conv > 0) {
         // ---- axial half-step: Lambda_r + X on the z-slabs, -> r-slabs, K-bar ----
         reset_status();
-        for (size_t lr = 0; lr < nl; ++lr) {
-          RankState& R = ranks[lr];
-          a[lr] = zdst(R, conv);
-          launch_rhs_zslab_exact(P, pulse, R.j0, R.nj, a[lr], R.zR, R.st, stream);
-          b[lr] = R.zR;
-          c[lr] = R.rHalf;
-          e[lr] = R.rExpl;
-        }
-        {
+        if (peer) {
+          // fused: T_half and Lambda_r + X stored straight into the owners' r-slabs
+          for (RankState& R : ranks)
+            launch_rhs_zslab_scatter(P, pulse, R.j0, R.nj, zdst(R, conv), ps, R.st, stream);
+          barrier();
+        } else {
+          for (size_t lr = 0; lr < nl; ++lr) {
+            RankState& R = ranks[lr];
+            a[lr] = zdst(R, conv);
+            launch_rhs_zslab_exact(P, pulse, R.j0, R.nj, a[lr], R.zR, R.st, stream);
+            b[lr] = R.zR;
+            c[lr] = R.rHalf;
+            e[lr] = R.rExpl;
+          }
           double* const* s2[2] = {a.data(), b.data()};
           double* const* d2[2] = {c.data(), e.data()};
           transpose_exact(true, 2, s2, d2);
@@ -482,7 +524,9 @@ struct pcgpu_dist {
         if (aconv < 0) return -aconv;
         *updates += static_cast<double>(active) * r->axial.iterations;
         if (aconv > 0) {
-          // accept: the r-slab result becomes the anchor; -> z-slabs
+          // accept: the r-slab result becomes the anchor (the next attempt's
+          // K3 moves it to the z-slabs: fused with the peer transport, here
+          // with the NCCL transport)
           for (size_t lr = 0; lr < nl; ++lr) {
             RankState& R = ranks[lr];
             double* res = rdst(R, aconv);
@@ -490,9 +534,11 @@ struct pcgpu_dist {
             a[lr] = R.rTc;
             b[lr] = R.zTc;
           }
-          double* const* s1[1] = {a.data()};
-          double* const* d1[1] = {b.data()};
-          transpose_exact(false, 1, s1, d1);
+          if (!peer) {
+            double* const* s1[1] = {a.data()};
+            double* const* d1[1] = {b.data()};
+            transpose_exact(false, 1, s1, d1);
+          }
           r->tau_used = tau;
           return PCGPU_OK;
         }
@@ -740,6 +786,16 @@ int pcgpu_dist_create(const pcgpu_desc* d, int32_t rank, int32_t nranks, const v
     DCK(cudaMemcpy(h->st_dev_list, sts.data(), sizeof(DevStatus*) * sts.size(),
                    cudaMemcpyHostToDevice));
     DCK(cudaMallocHost(&h->st_host, sizeof(DevStatus)));
+    DCK(cudaMalloc(&h->d_barrier, sizeof(unsigned long long)));
+    h->allocs.push_back(h->d_barrier);
+    DCK(cudaMemset(h->d_barrier, 0, sizeof(unsigned long long)));
+    if (nranks > kMaxPeers && d->mode == PCGPU_MODE_EXACT)
+      throw DistError{PCGPU_ERR_CONFIG, "pcgpu_dist: at most 16 ranks"};
+    if (h->local && d->mode == PCGPU_MODE_EXACT) {
+      const char* tr = std::getenv("PCGPU_DIST_TRANSPORT");
+      h->peer = !(tr && std::string(tr) == "nccl");
+      h->build_peer_table_local();
+    }
     DCK(cudaDeviceSynchronize());
   } catch (const DistError& e) {
     g_dist_create_error = e.what;
@@ -818,10 +874,12 @@ int pcgpu_dist_get_field(pcgpu_dist* h, double* fieldN) {
   try {
     const int nr = h->d.nr;
     for (RankState& R : h->ranks) {
-      if (h->exact())  // z-slab T layout -> N rows j0 .. j0+nj-1
-        transpose_block(R.zTc, R.nj, nr, R.nj, fieldN + static_cast<size_t>(R.j0) * nr, nr,
-                        h->stream);
-      else
+      if (h->exact()) {  // r-slab N layout [j][i - i0] -> columns i0 .. i0+ni-1
+        if (R.ni)
+          DCK(cudaMemcpy2DAsync(fieldN + R.i0, sizeof(double) * nr, R.rTc,
+                                sizeof(double) * R.ni, sizeof(double) * R.ni, h->d.nz,
+                                cudaMemcpyDeviceToDevice, h->stream));
+      } else
         DCK(cudaMemcpyAsync(fieldN + static_cast<size_t>(R.j0) * nr, R.zTc,
                             sizeof(double) * static_cast<size_t>(R.nj) * nr,
                             cudaMemcpyDeviceToDevice, h->stream));
@@ -864,6 +922,65 @@ int pcgpu_dist_run(pcgpu_dist* h, double t0, int32_t nsteps, pcgpu_step_result* 
   s.t_end = t;
   if (stats) *stats = s;
   return rc;
+}
+
+int32_t pcgpu_dist_transport(const pcgpu_dist* h) { return h->peer ? 1 : 0; }
+
+int pcgpu_dist_ipc_export(pcgpu_dist* h, void* handles) {
+  if (!h || !handles || !h->exact() || h->local) return PCGPU_ERR_ARG;
+  try {
+    RankState& R = h->ranks[0];
+    double* bufs[4] = {R.zTc, R.zExpl, R.rHalf, R.rExpl};
+    auto* out = static_cast<unsigned char*>(handles);
+    for (int k = 0; k < 4; ++k) {
+      cudaIpcMemHandle_t m;
+      DCK(cudaIpcGetMemHandle(&m, bufs[k]));
+      std::memcpy(out + k * sizeof m, &m, sizeof m);
+    }
+  } catch (const DistError& e) {
+    h->err = e.what;
+    return e.code;
+  }
+  return PCGPU_OK;
+}
+
+int pcgpu_dist_ipc_import(pcgpu_dist* h, const void* all_handles) {
+  if (!h || !all_handles || !h->exact() || h->local) return PCGPU_ERR_ARG;
+  try {
+    const auto* in = static_cast<const unsigned char*>(all_handles);
+    PeerSlabs ps{};
+    ps.nranks = h->nranks;
+    for (int q = 0; q <= h->nranks; ++q) {
+      ps.zb[q] = h->zb[q];
+      ps.rb[q] = h->rb[q];
+    }
+    const int me = h->ranks[0].rank;
+    for (int q = 0; q < h->nranks; ++q) {
+      double** dst[4] = {&ps.zTc[q], &ps.zExpl[q], &ps.rHalf[q], &ps.rExpl[q]};
+      if (q == me) {
+        RankState& R = h->ranks[0];
+        *dst[0] = R.zTc;
+        *dst[1] = R.zExpl;
+        *dst[2] = R.rHalf;
+        *dst[3] = R.rExpl;
+        continue;
+      }
+      for (int k = 0; k < 4; ++k) {
+        cudaIpcMemHandle_t m;
+        std::memcpy(&m, in + (static_cast<size_t>(q) * 4 + k) * sizeof m, sizeof m);
+        void* p = nullptr;
+        DCK(cudaIpcOpenMemHandle(&p, m, cudaIpcMemLazyEnablePeerAccess));
+        h->ipc_opened.push_back(p);
+        *dst[k] = static_cast<double*>(p);
+      }
+    }
+    h->ps = ps;
+    h->peer = true;
+  } catch (const DistError& e) {
+    h->err = e.what;
+    return e.code;
+  }
+  return PCGPU_OK;
 }
 
 void* pcgpu_dist_stream(const pcgpu_dist* h) { return h->stream; }

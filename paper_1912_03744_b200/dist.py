@@ -122,6 +122,29 @@ class PartitionedAdi:
         self._check(rc)
         return float(st.t_end), stats, ([_step_result(r) for r in res] if res is not None else [])
 
+    def transport(self) -> str:
+        """'peer' (fused slab passes store into the owners' slabs) or 'nccl'
+        (all-to-all transposes)."""
+        return "peer" if self._lib.pcgpu_dist_transport(self._h) == 1 else "nccl"
+
+    def enable_peer_transport(self) -> None:
+        """Exact mode, one process per GPU: map every rank's slabs into this
+        process (CUDA IPC handles all-gathered over torch.distributed), so the
+        fused K3/K4 passes store straight into the peers over NVLink."""
+        import torch
+        import torch.distributed as dist
+        mine = (C.c_uint8 * N.DIST_IPC_BYTES)()
+        self._check(self._lib.pcgpu_dist_ipc_export(self._h, mine))
+        t = torch.frombuffer(bytearray(bytes(mine)), dtype=torch.uint8)
+        world = dist.get_world_size()
+        dev = f"cuda:{torch.cuda.current_device()}" if dist.get_backend() == "nccl" else "cpu"
+        parts = [torch.zeros(N.DIST_IPC_BYTES, dtype=torch.uint8, device=dev)
+                 for _ in range(world)]
+        dist.all_gather(parts, t.to(dev))
+        blob = b"".join(bytes(p.cpu().numpy().tobytes()) for p in parts)
+        allh = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        self._check(self._lib.pcgpu_dist_ipc_import(self._h, allh))
+
     def stream(self) -> int:
         return int(self._lib.pcgpu_dist_stream(self._h) or 0)
 

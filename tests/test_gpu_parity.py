@@ -416,8 +416,11 @@ def test_fast_vs_exact_cfg3_full_size(cuda):
 @pytest.mark.parametrize("name,nranks,steps", [
     ("cfg0", 2, 30), ("cfg0", 3, 30), ("cfg4s", 4, 6), ("cfg4s", 8, 6), ("cfg4s", 1, 4),
 ])
-def test_partitioned_exact_emulated_bitwise(cuda, name, nranks, steps):
+@pytest.mark.parametrize("transport", ["peer", "nccl"])
+def test_partitioned_exact_emulated_bitwise(cuda, name, nranks, steps, transport, monkeypatch):
     from paper_1912_03744_b200.dist import PartitionedAdi
+    if transport == "nccl":  # all-to-all transposes (memcpy stand-ins when emulated)
+        monkeypatch.setenv("PCGPU_DIST_TRANSPORT", "nccl")
     case = configs.cfg0() if name == "cfg0" else \
         configs.scaled(configs.cfg4(), [706, 71, 212, 35], 2048, 1400)
     g = case.grid()
@@ -436,8 +439,10 @@ def test_partitioned_exact_emulated_bitwise(cuda, name, nranks, steps):
     assert _seq(r1).tolist() == _seq(r2).tolist()
     m = g.mask()
     assert np.array_equal(to_host(out)[m], to_host(f1)[m])
+    assert part.transport() == transport
     tm = part.timing()
-    assert tm["transposes"] == 3 * steps and tm["allreduces"] > 0
+    assert tm["transposes"] == (3 * steps if transport == "nccl" else 0)
+    assert tm["allreduces"] > 0
 
 
 def test_partitioned_exact_halving_and_clamps_vs_oracle(cuda):
