@@ -235,6 +235,66 @@ int64_t pcgpu_launch_count(const pcgpu_stepper* h);
  * len bytes). Returns the full length. */
 int32_t pcgpu_describe(const pcgpu_stepper* h, char* buf, int32_t len);
 
+/* ---- Device-resident runner -------------------------------
+ * pulsecell::evolve (runner.cpp:97-190) with the field resident on the
+ * device: steps from t = 0 (Kahan-accumulated time) until t_end, the
+ * periodic-regime detector fires, or the step hits its floor. Per step only
+ * the probe values come back (a device gather); snapshots are handed to the
+ * caller as device pointers valid during the callback; the pre-turn-on
+ * capture copies the field on the device only for steps that can cross a
+ * period boundary. The regime detector (PhaseResampler / RegimeDetector,
+ * runner.cpp:35-95) runs on the host over probe 0. Probe cells are the
+ * caller's pulsecell::probe_cell(grid, r, z) (runner.cpp:20-28). */
+typedef struct pcgpu_runner_cfg {
+  double t_end;
+  int32_t n_probes;
+  const int32_t* probe_i; /* radial cell of each probe */
+  const int32_t* probe_j; /* axial cell of each probe */
+  int32_t n_snapshot_times;
+  const double* snapshot_times; /* any order (sorted by the runner) */
+  int32_t snapshot_pre_on;
+  int32_t snapshot_post_off;
+  int32_t detector_samples_per_period;
+  int32_t detector_min_periods;
+  double detector_tolerance;
+  int32_t source_on; /* SourceSpec::I0 > 0: regime detection engages with >= 1 probe */
+} pcgpu_runner_cfg;
+
+typedef enum { PCGPU_STOP_REACHED_TIME = 0, PCGPU_STOP_PERIODIC = 1, PCGPU_STOP_TAU_FLOOR = 2 } pcgpu_stop;
+typedef enum { PCGPU_SNAP_PRE_ON = 0, PCGPU_SNAP_POST_OFF = 1, PCGPU_SNAP_AT_TIME = 2 } pcgpu_snap;
+
+/* Called after every accepted step with the step count, t, tau_used and the
+ * n_probes probe values (TraceEntry, runner.hpp:29-33). */
+typedef void (*pcgpu_step_cb)(void* user, int64_t step, double t, double tau,
+                              const double* probe_values);
+/* Snapshot (runner.hpp:106-109): field_dev is an nr x nz column-major device
+ * field valid until the callback returns. */
+typedef void (*pcgpu_snapshot_cb)(void* user, int32_t kind, double t, const double* field_dev);
+
+typedef struct pcgpu_evolve_result {
+  double t;
+  int64_t steps;
+  int32_t reason; /* pcgpu_stop */
+  double fire_t;  /* -1 unless the detector fired */
+  int32_t detector_periods; /* completed resampled periods of probe 0 */
+} pcgpu_evolve_result;
+
+/* field_dev is the initial field in, the final field out (the last accepted
+ * one on a TauFloor stop; pcgpu_last_error() holds the reason). Returns
+ * PCGPU_OK for all three stop reasons. */
+int pcgpu_evolve(pcgpu_stepper* h, double* field_dev, const pcgpu_runner_cfg* cfg,
+                 pcgpu_step_cb on_step, pcgpu_snapshot_cb on_snapshot, void* user,
+                 pcgpu_evolve_result* result);
+/* Host-field variant (for callers without CUDA, e.g. the C++ drop-in's
+ * evolve): the field is copied in and out, and snapshots are handed over as
+ * host nr x nz column-major fields valid during the callback. */
+int pcgpu_evolve_host(pcgpu_stepper* h, double* field_host, const pcgpu_runner_cfg* cfg,
+                      pcgpu_step_cb on_step, pcgpu_snapshot_cb on_snapshot, void* user,
+                      pcgpu_evolve_result* result);
+/* The last evolve's resampled periods of probe 0 (detector_periods rows of
+ * detector_samples_per_period values), into rows (capacity max_rows). */
+int pcgpu_detector_periods(const pcgpu_stepper* h, double* rows, int32_t max_rows);
+
 /* ---- Partitioned stepper: one node of B200s ------------------
  * z-slabs (radial lines j) for the radial sweep, r-slabs (axial lines i) for
  * the axial sweep, all-to-all transposes between them, allreduce(max) of the

@@ -24,6 +24,7 @@
 #include "pulsecell/errors.hpp"
 #include "pulsecell/geometry.hpp"
 #include "pulsecell/materials.hpp"
+#include "pulsecell/runner.hpp"
 #include "pulsecell/solver.hpp"
 #include "pulsecell/source.hpp"
 
@@ -178,6 +179,79 @@ class AdiStepper {
   std::vector<pcgpu_material> mat_;
   pcgpu_stepper* h_ = nullptr;
 };
+
+/// pulsecell::evolve (runner.cpp:97-190) for the GPU stepper, with the same
+/// arguments and EvolutionResult: the field stays on the device for the whole
+/// run (pcgpu_evolve_host); only probe values cross each step and snapshots
+/// when they occur. The probe cells are the reference's own probe_cell.
+inline EvolutionResult evolve(AdiStepper& stepper, const SourceSpec& timing, Array2 initial,
+                              Real t_end, const RunnerConfig& cfg) {
+  cfg.validate();
+  const Grid& grid = stepper.grid();
+  std::vector<int32_t> pi, pj;
+  for (const auto& p : cfg.probes) {
+    const auto c = probe_cell(grid, p.r, p.z);
+    pi.push_back(static_cast<int32_t>(c.first));
+    pj.push_back(static_cast<int32_t>(c.second));
+  }
+  pcgpu_runner_cfg c{};
+  c.t_end = t_end;
+  c.n_probes = static_cast<int32_t>(pi.size());
+  c.probe_i = pi.data();
+  c.probe_j = pj.data();
+  c.n_snapshot_times = static_cast<int32_t>(cfg.snapshot_times.size());
+  c.snapshot_times = cfg.snapshot_times.data();
+  c.snapshot_pre_on = cfg.snapshot_pre_on;
+  c.snapshot_post_off = cfg.snapshot_post_off;
+  c.detector_samples_per_period = cfg.detector.samples_per_period;
+  c.detector_min_periods = cfg.detector.min_periods;
+  c.detector_tolerance = cfg.detector.tolerance;
+  c.source_on = timing.I0 > 0;
+  EvolutionResult res;
+  res.field = std::move(initial);
+  struct Sink {
+    EvolutionResult* r;
+    const Grid* g;
+    size_t np;
+  } sink{&res, &grid, pi.size()};
+  auto on_step = [](void* u, int64_t, double t, double tau, const double* v) {
+    Sink* s = static_cast<Sink*>(u);
+    TraceEntry e;
+    e.t = t;
+    e.tau = tau;
+    e.values.assign(v, v + s->np);
+    s->r->trace.push_back(std::move(e));
+  };
+  auto on_snap = [](void* u, int32_t kind, double t, const double* f) {
+    Sink* s = static_cast<Sink*>(u);
+    Array2 a(s->g->nr(), s->g->nz());
+    std::memcpy(a.data(), f, sizeof(double) * a.size());
+    Snapshot snap{t, std::move(a)};
+    if (kind == PCGPU_SNAP_PRE_ON) s->r->pre_on = std::move(snap);
+    else if (kind == PCGPU_SNAP_POST_OFF) s->r->post_off = std::move(snap);
+    else s->r->at_times.push_back(std::move(snap));
+  };
+  pcgpu_evolve_result out{};
+  const int rc = pcgpu_evolve_host(stepper.handle(), res.field.data(), &c, on_step, on_snap,
+                                   &sink, &out);
+  if (rc != PCGPU_OK) throw Error(std::string("pcgpu_evolve: ") + pcgpu_last_error(stepper.handle()));
+  res.t = out.t;
+  res.steps = out.steps;
+  res.reason = static_cast<StopReason>(out.reason);
+  res.fire_t = out.fire_t;
+  if (res.reason == StopReason::TauFloor) res.error = pcgpu_last_error(stepper.handle());
+  if (out.detector_periods > 0) {
+    const int s = cfg.detector.samples_per_period;
+    std::vector<double> rows(static_cast<size_t>(out.detector_periods) * s);
+    pcgpu_detector_periods(stepper.handle(), rows.data(), out.detector_periods);
+    for (int k = 0; k < out.detector_periods; ++k) {
+      Vector v(s);
+      for (int q = 0; q < s; ++q) v[q] = rows[static_cast<size_t>(k) * s + q];
+      res.detector_periods.push_back(std::move(v));
+    }
+  }
+  return res;
+}
 
 }  // namespace gpu
 }  // namespace pulsecell

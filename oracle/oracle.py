@@ -46,6 +46,25 @@ class RefSpec(C.Structure):
     ]
 
 
+class RefEvolveIO(C.Structure):
+    """pcref_evolve_io (oracle/ref_bridge.h)."""
+    _fields_ = [
+        ("t_end", C.c_double), ("n_probes", C.c_int32), ("probe_r", _dp), ("probe_z", _dp),
+        ("n_snapshot_times", C.c_int32), ("snapshot_times", _dp),
+        ("snapshot_pre_on", C.c_int32), ("snapshot_post_off", C.c_int32),
+        ("detector_samples_per_period", C.c_int32), ("detector_min_periods", C.c_int32),
+        ("detector_tolerance", C.c_double), ("I0", C.c_double),
+        ("t", C.c_double), ("fire_t", C.c_double), ("steps", C.c_int64), ("reason", C.c_int32),
+        ("trace_cap", C.c_int64), ("trace_t", _dp), ("trace_tau", _dp), ("trace_values", _dp),
+        ("has_pre_on", C.c_int32), ("has_post_off", C.c_int32),
+        ("pre_on_t", C.c_double), ("post_off_t", C.c_double),
+        ("pre_on_field", _dp), ("post_off_field", _dp),
+        ("at_cap", C.c_int32), ("at_count", C.c_int32), ("at_t", _dp), ("at_fields", _dp),
+        ("det_cap", C.c_int32), ("det_rows", C.c_int32), ("det_values", _dp),
+        ("probe_i", C.c_int32 * 16), ("probe_j", C.c_int32 * 16),
+    ]
+
+
 _port = None
 _ref = None
 
@@ -111,6 +130,7 @@ def _load_ref():
             ("pcref_axial_half_step", C.c_int, [_vp, _vp, C.c_double, C.c_double, _vp, O]),
             ("pcref_step", C.c_int, [_vp, _vp, C.c_double, S]),
             ("pcref_run", C.c_int, [_vp, _vp, C.c_double, C.c_int32, S, R]),
+            ("pcref_evolve", C.c_int, [_vp, _vp, C.POINTER(RefEvolveIO)]),
             ("pcref_clamp_events", C.c_int, [_vp, C.POINTER(C.c_uint64)]),
             ("pcref_apply_lambda_r", C.c_double, [_vp, _vp, C.c_int64, C.c_int64]),
             ("pcref_apply_lambda_z", C.c_double, [_vp, _vp, C.c_int64, C.c_int64]),
@@ -186,6 +206,53 @@ class _Base:
 
     def pulse_value(self, t):
         return float(self._call("pulse_value", t))
+
+
+def ref_evolve(ref: "RefStepper", field: np.ndarray, t_end: float, cfg, I0: float,
+               trace_cap: int = 200000, at_cap: int = 16, det_cap: int = 4096):
+    """pulsecell::evolve of the reference itself (runner.cpp:97-190). Returns a
+    dict: field (in place), t, steps, reason, fire_t, trace (t, tau, values),
+    pre_on / post_off (t, field) or None, at_times [(t, field)], detector rows,
+    and the probe cells the reference chose."""
+    nr, nz = field.shape
+    cells = nr * nz
+    npr = len(cfg.probes)
+    pr = np.array([p.r for p in cfg.probes] or [0.0])
+    pz = np.array([p.z for p in cfg.probes] or [0.0])
+    st = np.array(cfg.snapshot_times or [0.0])
+    tt, ttau = np.zeros(trace_cap), np.zeros(trace_cap)
+    tv = np.zeros(trace_cap * max(1, npr))
+    pre, post = np.zeros(cells), np.zeros(cells)
+    at_t, at_f = np.zeros(at_cap), np.zeros(at_cap * cells)
+    s = cfg.detector.samples_per_period
+    dv = np.zeros(det_cap * s)
+    io = RefEvolveIO()
+    io.t_end, io.n_probes = t_end, npr
+    io.probe_r, io.probe_z = pr.ctypes.data_as(_dp), pz.ctypes.data_as(_dp)
+    io.n_snapshot_times, io.snapshot_times = len(cfg.snapshot_times), st.ctypes.data_as(_dp)
+    io.snapshot_pre_on, io.snapshot_post_off = int(cfg.snapshot_pre_on), int(cfg.snapshot_post_off)
+    io.detector_samples_per_period, io.detector_min_periods = s, cfg.detector.min_periods
+    io.detector_tolerance, io.I0 = cfg.detector.tolerance, I0
+    io.trace_cap = trace_cap
+    io.trace_t, io.trace_tau, io.trace_values = (a.ctypes.data_as(_dp) for a in (tt, ttau, tv))
+    io.pre_on_field, io.post_off_field = pre.ctypes.data_as(_dp), post.ctypes.data_as(_dp)
+    io.at_cap, io.at_t, io.at_fields = at_cap, at_t.ctypes.data_as(_dp), at_f.ctypes.data_as(_dp)
+    io.det_cap, io.det_values = det_cap, dv.ctypes.data_as(_dp)
+    ref._check(ref.lib.pcref_evolve(ref.h, _ptr(field), C.byref(io)))
+    n = int(io.steps)
+    assert n <= trace_cap
+    shape = (nr, nz)
+    return {
+        "t": io.t, "steps": n, "reason": int(io.reason), "fire_t": io.fire_t,
+        "trace": [(tt[k], ttau[k], list(tv[k * npr:(k + 1) * npr])) for k in range(n)],
+        "pre_on": (io.pre_on_t, pre.reshape(shape, order="F")) if io.has_pre_on else None,
+        "post_off": (io.post_off_t, post.reshape(shape, order="F")) if io.has_post_off else None,
+        "at_times": [(at_t[k], at_f[k * cells:(k + 1) * cells].reshape(shape, order="F"))
+                     for k in range(min(io.at_count, at_cap))],
+        "detector": [dv[k * s:(k + 1) * s].copy() for k in range(min(io.det_rows, det_cap))],
+        "probe_cells": [(io.probe_i[k], io.probe_j[k]) for k in range(min(npr, 16))],
+        "error": ref.lib.pcref_last_error(ref.h).decode() if io.reason == 2 else "",
+    }
 
 
 class OracleError(RuntimeError):

@@ -16,6 +16,7 @@
 #include "pulsecell/geometry.hpp"
 #include "pulsecell/materials.hpp"
 #include "pulsecell/parallel.hpp"
+#include "pulsecell/runner.hpp"
 #include "pulsecell/solver.hpp"
 #include "pulsecell/source.hpp"
 #include "pulsecell/tridiagonal.hpp"
@@ -262,6 +263,66 @@ int pcref_step(pcref* h, double* field, double t, pcgpu_step_result* result) {
 // nsteps x step() with t += tau_used, exactly the bench harness loop
 // (bench.cpp:20-22). Stats count the accepted attempt's iterations (step()
 // reports only those, solver.hpp:56-60).
+int pcref_evolve(pcref* h, double* field, pcref_evolve_io* io) {
+  try {
+    RunnerConfig rc;
+    rc.t_end = io->t_end;
+    rc.detector.samples_per_period = io->detector_samples_per_period;
+    rc.detector.min_periods = io->detector_min_periods;
+    rc.detector.tolerance = io->detector_tolerance;
+    for (int32_t k = 0; k < io->n_probes; ++k) {
+      rc.probes.push_back(ProbeSpec{io->probe_r[k], io->probe_z[k]});
+      const auto c = probe_cell(*h->grid, io->probe_r[k], io->probe_z[k]);
+      if (k < 16) {
+        io->probe_i[k] = static_cast<int32_t>(c.first);
+        io->probe_j[k] = static_cast<int32_t>(c.second);
+      }
+    }
+    rc.snapshot_times.assign(io->snapshot_times, io->snapshot_times + io->n_snapshot_times);
+    rc.snapshot_pre_on = io->snapshot_pre_on != 0;
+    rc.snapshot_post_off = io->snapshot_post_off != 0;
+    SourceSpec timing = h->timing;
+    timing.I0 = io->I0;
+    EvolutionResult r = evolve(*h->stepper, timing, to_array(h, field), io->t_end, rc);
+    std::memcpy(field, r.field.data(), sizeof(double) * r.field.size());
+    io->t = r.t;
+    io->steps = r.steps;
+    io->reason = static_cast<int32_t>(r.reason);
+    io->fire_t = r.fire_t;
+    const size_t cells = static_cast<size_t>(r.field.size());
+    for (size_t k = 0; k < r.trace.size() && static_cast<int64_t>(k) < io->trace_cap; ++k) {
+      io->trace_t[k] = r.trace[k].t;
+      io->trace_tau[k] = r.trace[k].tau;
+      for (int32_t p = 0; p < io->n_probes; ++p)
+        io->trace_values[k * io->n_probes + p] = r.trace[k].values[p];
+    }
+    io->has_pre_on = r.pre_on.has_value();
+    if (r.pre_on) {
+      io->pre_on_t = r.pre_on->t;
+      if (io->pre_on_field) std::memcpy(io->pre_on_field, r.pre_on->field.data(), sizeof(double) * cells);
+    }
+    io->has_post_off = r.post_off.has_value();
+    if (r.post_off) {
+      io->post_off_t = r.post_off->t;
+      if (io->post_off_field)
+        std::memcpy(io->post_off_field, r.post_off->field.data(), sizeof(double) * cells);
+    }
+    io->at_count = static_cast<int32_t>(r.at_times.size());
+    for (int32_t k = 0; k < io->at_count && k < io->at_cap; ++k) {
+      io->at_t[k] = r.at_times[k].t;
+      std::memcpy(io->at_fields + k * cells, r.at_times[k].field.data(), sizeof(double) * cells);
+    }
+    io->det_rows = static_cast<int32_t>(r.detector_periods.size());
+    for (int32_t k = 0; k < io->det_rows && k < io->det_cap; ++k)
+      for (int32_t q = 0; q < io->detector_samples_per_period; ++q)
+        io->det_values[k * io->detector_samples_per_period + q] = r.detector_periods[k][q];
+    if (r.reason == StopReason::TauFloor) h->error = r.error;
+  } catch (const std::exception& e) {
+    return h->fail(e);
+  }
+  return PCGPU_OK;
+}
+
 int pcref_run(pcref* h, double* field, double t0, int32_t nsteps, pcgpu_step_result* results,
               pcgpu_run_stats* stats) {
   pcgpu_run_stats st{};

@@ -68,6 +68,37 @@ int pcref_run(pcref* h, double* field, double t0, int32_t nsteps, pcgpu_step_res
               pcgpu_run_stats* stats);
 int pcref_clamp_events(const pcref* h, uint64_t* counts);
 
+/* pulsecell::evolve (runner.cpp:97-190) on the reference stepper, with
+ * probes at (r, z). field: initial in, final out. Trace arrays hold
+ * trace_cap entries (values: trace_cap x n_probes); snapshot fields nr*nz. */
+typedef struct pcref_evolve_io {
+  double t_end;
+  int32_t n_probes;
+  const double* probe_r;
+  const double* probe_z;
+  int32_t n_snapshot_times;
+  const double* snapshot_times;
+  int32_t snapshot_pre_on, snapshot_post_off;
+  int32_t detector_samples_per_period, detector_min_periods;
+  double detector_tolerance;
+  double I0; /* SourceSpec::I0 (the detector engages only when > 0) */
+  /* outputs */
+  double t, fire_t;
+  int64_t steps;
+  int32_t reason;
+  int64_t trace_cap;
+  double *trace_t, *trace_tau, *trace_values;
+  int32_t has_pre_on, has_post_off;
+  double pre_on_t, post_off_t;
+  double *pre_on_field, *post_off_field;
+  int32_t at_cap, at_count;
+  double *at_t, *at_fields;
+  int32_t det_cap, det_rows;
+  double* det_values; /* det_cap x samples */
+  int32_t probe_i[16], probe_j[16]; /* probe_cell of each probe (<= 16) */
+} pcref_evolve_io;
+int pcref_evolve(pcref* h, double* field, pcref_evolve_io* io);
+
 /* Operators and diagnostics (solver.cpp:53-119). */
 double pcref_apply_lambda_r(const pcref* h, const double* field, int64_t i, int64_t j);
 double pcref_apply_lambda_z(const pcref* h, const double* field, int64_t i, int64_t j);

@@ -22,8 +22,15 @@ OK, ERR_CONFIG, ERR_TAU_FLOOR, ERR_TABLE_RANGE, ERR_ZERO_PIVOT, ERR_CUDA, ERR_AR
 MODE_EXACT, MODE_FAST = 0, 1
 SOURCE_NULL, SOURCE_JOULE, SOURCE_FIELD = 0, 1, 2
 LAYOUT_CONTIGUOUS, LAYOUT_STRIDED = 0, 1
+STOP_REACHED_TIME, STOP_PERIODIC, STOP_TAU_FLOOR = 0, 1, 2
+SNAP_PRE_ON, SNAP_POST_OFF, SNAP_AT_TIME = 0, 1, 2
 
 _dp = C.POINTER(C.c_double)
+
+# pcgpu_evolve callbacks (include/pcgpu.h)
+STEP_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_double, C.c_double,
+                      C.POINTER(C.c_double))
+SNAP_CB = C.CFUNCTYPE(None, C.c_void_p, C.c_int32, C.c_double, C.c_void_p)
 
 
 class Table(C.Structure):
@@ -81,7 +88,8 @@ EXPORTS = [
     "pcgpu_dist_last_error", "pcgpu_dist_plan", "pcgpu_dist_slabs", "pcgpu_dist_set_field",
     "pcgpu_dist_get_field", "pcgpu_dist_run", "pcgpu_dist_stream", "pcgpu_dist_enable_timing",
     "pcgpu_dist_timing", "pcgpu_dist_launch_count", "pcgpu_run_growth", "pcgpu_describe", "pcgpu_dist_transport",
-    "pcgpu_dist_ipc_export", "pcgpu_dist_ipc_import",
+    "pcgpu_dist_ipc_export", "pcgpu_dist_ipc_import", "pcgpu_evolve", "pcgpu_detector_periods",
+    "pcgpu_evolve_host",
 ]
 
 _lib = None
@@ -131,6 +139,9 @@ def load():
         "pcgpu_enable_kernel_timing": (C.c_int, [vp, C.c_int32]),
         "pcgpu_launch_count": (C.c_int64, [vp]),
         "pcgpu_describe": (C.c_int32, [vp, C.c_char_p, C.c_int32]),
+        "pcgpu_evolve": (C.c_int, [vp, vp, vp, STEP_CB, SNAP_CB, vp, vp]),
+        "pcgpu_detector_periods": (C.c_int, [vp, vp, C.c_int32]),
+        "pcgpu_evolve_host": (C.c_int, [vp, vp, vp, STEP_CB, SNAP_CB, vp, vp]),
         "pcgpu_tridiag_batch": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, C.c_int64, C.c_int32,
                                           C.c_int32, vp, C.POINTER(C.c_int64)]),
         "pcgpu_nccl_unique_id": (C.c_int, [vp]),

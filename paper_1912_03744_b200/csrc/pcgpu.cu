@@ -154,8 +154,15 @@ enum Buf {
   kNumBufs
 };
 
+// The last evolve's resampled probe-0 periods (pcgpu_detector_periods).
+struct pcgpu_runner_state {
+  std::vector<std::vector<double>> detector_rows;
+  int samples = 0;
+};
+
 struct pcgpu_stepper {
   pcgpu_desc d{};
+  pcgpu_runner_state* runner = nullptr;  // the last evolve's detector rows
   DevProblem P{};
   std::vector<void*> dev_allocs;
   cudaStream_t stream = nullptr;
@@ -179,6 +186,7 @@ struct pcgpu_stepper {
   unsigned long long launches0 = 0;
 
   ~pcgpu_stepper() {
+    delete runner;
     if (stream) cudaStreamSynchronize(stream);
     for (auto& e : ev_pool) cudaEventDestroy(e);
     for (void* p : dev_allocs) cudaFree(p);
@@ -1080,6 +1088,296 @@ int pcgpu_kernel_timing(const pcgpu_stepper* h, double* radial_ms, int64_t* radi
   *radial_launches = h->radial_launches;
   *axial_ms = h->axial_ms;
   *axial_launches = h->axial_launches;
+  return PCGPU_OK;
+}
+
+}  // extern "C"
+
+// ---- Device-resident runner --------------------------------
+namespace {
+
+// PhaseResampler (runner.cpp:35-62): resamples an adaptively stepped trace
+// onto samples_per_period fixed phases of each period by linear interpolation.
+struct PhaseResamplerGpu {
+  double t_per = 1, dt = 1;
+  int samples = 1;
+  long next_sample = 0;
+  bool seeded = false;
+  double t_prev = 0, v_prev = 0;
+  std::vector<double> current;
+  std::vector<std::vector<double>> rows;
+  PhaseResamplerGpu(double tp, int s) : t_per(tp), dt(tp / s), samples(s), current(s, 0.0) {}
+  void seed(double t, double v) {
+    t_prev = t;
+    v_prev = v;
+    seeded = true;
+    next_sample = static_cast<long>(std::ceil(t / dt));
+  }
+  void feed(double t, double v) {
+    if (!seeded) {
+      seed(t, v);
+      return;
+    }
+    while (static_cast<double>(next_sample) * dt <= t) {
+      const double pt = static_cast<double>(next_sample) * dt;
+      double val = v_prev;
+      if (t > t_prev) val = v_prev + (v - v_prev) * ((pt - t_prev) / (t - t_prev));
+      current[next_sample % samples] = val;
+      if (next_sample % samples == samples - 1) rows.push_back(current);
+      ++next_sample;
+    }
+    t_prev = t;
+    v_prev = v;
+  }
+};
+
+// RegimeDetector::update (runner.cpp:76-95): fires once `min_periods`
+// consecutive period pairs agree phase-wise within `tol` (max |difference|,
+// NaN-ignoring maximum like the reference's reduction).
+struct RegimeDetectorGpu {
+  PhaseResamplerGpu rs;
+  double tol;
+  int min_periods;
+  size_t checked = 1;
+  int consecutive = 0;
+  bool fired = false;
+  RegimeDetectorGpu(double tp, int samples, double tol_, int minp)
+      : rs(tp, samples), tol(tol_), min_periods(minp) {}
+  bool update(double t, double v) {
+    rs.feed(t, v);
+    while (checked < rs.rows.size()) {
+      const std::vector<double>& a = rs.rows[checked];
+      const std::vector<double>& b = rs.rows[checked - 1];
+      double diff = std::abs(a[0] - b[0]);
+      for (size_t q = 1; q < a.size(); ++q) {
+        const double d = std::abs(a[q] - b[q]);
+        if (diff < d) diff = d;
+      }
+      consecutive = diff < tol ? consecutive + 1 : 0;
+      ++checked;
+      if (!fired && consecutive >= min_periods) {
+        fired = true;
+        return true;
+      }
+    }
+    return false;
+  }
+};
+
+__global__ void k_gather_probes(const double* __restrict__ f, const int* __restrict__ off, int n,
+                                double* __restrict__ out) {
+  const int k = threadIdx.x;
+  if (k < n) out[k] = f[off[k]];
+}
+
+}  // namespace
+
+extern "C" {
+
+int pcgpu_evolve(pcgpu_stepper* h, double* field, const pcgpu_runner_cfg* cfg,
+                 pcgpu_step_cb on_step, pcgpu_snapshot_cb on_snapshot, void* user,
+                 pcgpu_evolve_result* res) {
+  if (!h || !field || !cfg || !res) return PCGPU_ERR_ARG;
+  // RunnerConfig::validate (runner.hpp:96-102)
+  if (!(cfg->t_end > 0)) return h->fail(PCGPU_ERR_CONFIG, "runner.t_end: must be > 0");
+  if (cfg->detector_samples_per_period < 1)
+    return h->fail(PCGPU_ERR_CONFIG, "detector.samples_per_period: must be >= 1");
+  if (!(cfg->detector_tolerance > 0))
+    return h->fail(PCGPU_ERR_CONFIG, "detector.tolerance: must be > 0");
+  if (cfg->detector_min_periods < 1)
+    return h->fail(PCGPU_ERR_CONFIG, "detector.min_periods: must be >= 1");
+  std::vector<double> pending(cfg->snapshot_times, cfg->snapshot_times + cfg->n_snapshot_times);
+  for (double ts : pending)
+    if (ts < 0) return h->fail(PCGPU_ERR_CONFIG, "runner.snapshot_times: must be >= 0");
+  std::sort(pending.begin(), pending.end());
+  const int np = cfg->n_probes;
+  if (np < 0 || np > 1024) return PCGPU_ERR_ARG;
+  const pcgpu_desc& d = h->d;
+  std::vector<int> off(np);
+  for (int k = 0; k < np; ++k) {
+    const int i = cfg->probe_i[k], j = cfg->probe_j[k];
+    const bool in_mask = i >= 0 && i < d.nr && j >= 0 &&
+                         j < (i < d.nr_core ? d.nz : d.nz_shared);
+    if (!in_mask) return h->fail(PCGPU_ERR_CONFIG, "probe cell falls outside the domain");
+    off[k] = h->fast() ? i * d.nz + j : j * d.nr + i;  // state layout
+  }
+  *res = pcgpu_evolve_result{};
+  res->fire_t = -1;
+  GUARD_BEGIN
+  int* d_off = nullptr;
+  double* d_vals = nullptr;
+  double* h_vals = nullptr;
+  CK(cudaMalloc(&d_off, sizeof(int) * std::max(np, 1)));
+  CK(cudaMalloc(&d_vals, sizeof(double) * std::max(np, 1)));
+  CK(cudaMallocHost(&h_vals, sizeof(double) * std::max(np, 1)));
+  struct Free {
+    int* a;
+    double* b;
+    double* c;
+    ~Free() {
+      cudaFree(a);
+      cudaFree(b);
+      cudaFreeHost(c);
+    }
+  } free_guard{d_off, d_vals, h_vals};
+  if (np) CK(cudaMemcpy(d_off, off.data(), sizeof(int) * np, cudaMemcpyHostToDevice));
+  double* cur = h->buf[kField];
+  double* nxt = h->buf[kNext];
+  double* spare = h->buf[kIterT];
+  h->to_state(field, cur);
+  auto probes = [&](const double* state) {
+    if (!np) return;
+    k_gather_probes<<<1, 1024, 0, h->stream>>>(state, d_off, np, d_vals);
+    ++g_launches;
+    CK(cudaMemcpyAsync(h_vals, d_vals, sizeof(double) * np, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  };
+  // snapshots leave through the user layout (N): the state itself in exact
+  // mode, a transposed copy in fast mode
+  auto snapshot = [&](int kind, double ts, const double* state) {
+    if (!on_snapshot) return;
+    const double* f = state;
+    if (h->fast()) {
+      ensure_stage(h);
+      h->from_state(state, h->buf[kStage]);
+      f = h->buf[kStage];
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    on_snapshot(user, kind, ts, f);
+  };
+  const bool detect = cfg->source_on && np > 0;
+  RegimeDetectorGpu det(d.t_per, cfg->detector_samples_per_period, cfg->detector_tolerance,
+                        cfg->detector_min_periods);
+  if (detect) {
+    probes(cur);
+    det.rs.seed(0.0, h_vals[0]);
+  }
+  long period_idx = 1, off_idx = 0;
+  const double off_offset = d.t_src + d.t_trs;
+  size_t next_time = 0;
+  double t = 0, comp = 0;
+  int stop = PCGPU_STOP_REACHED_TIME;
+  for (;;) {
+    if (t >= cfg->t_end) {
+      stop = PCGPU_STOP_REACHED_TIME;
+      break;
+    }
+    const double t_before = t;
+    pcgpu_step_result r;
+    const double* acc = nullptr;
+    double upd = 0;
+    h->buf[kIterT] = spare;
+    const int rc = h->step(cur, t, nxt, &acc, &r, &upd);
+    if (rc == PCGPU_ERR_TAU_FLOOR) {  // the field stays the last accepted one
+      stop = PCGPU_STOP_TAU_FLOOR;
+      break;
+    }
+    if (rc) {
+      h->buf[kField] = cur;
+      h->buf[kNext] = nxt;
+      h->buf[kIterT] = spare;
+      return rc;
+    }
+    // Kahan accumulation of the accepted steps (runner.cpp:141-146)
+    {
+      const double y = r.tau_used - comp;
+      const double tt = t + y;
+      comp = (tt - t) - y;
+      t = tt;
+    }
+    res->steps += 1;
+    double* prev = cur;  // the step's input stays intact until the next step
+    cur = const_cast<double*>(acc);
+    if (cur == nxt) nxt = prev; else spare = prev;
+    probes(cur);
+    if (on_step) on_step(user, res->steps, t, r.tau_used, h_vals);
+    const double edge = static_cast<double>(period_idx) * d.t_per;
+    if (cfg->snapshot_pre_on && t >= edge && t_before < edge)
+      snapshot(PCGPU_SNAP_PRE_ON, t_before, prev);
+    while (t >= static_cast<double>(period_idx) * d.t_per) ++period_idx;
+    if (cfg->snapshot_post_off && t >= static_cast<double>(off_idx) * d.t_per + off_offset) {
+      snapshot(PCGPU_SNAP_POST_OFF, t, cur);
+      while (t >= static_cast<double>(off_idx) * d.t_per + off_offset) ++off_idx;
+    }
+    while (next_time < pending.size() && t >= pending[next_time]) {
+      snapshot(PCGPU_SNAP_AT_TIME, t, cur);
+      ++next_time;
+    }
+    if (detect && det.update(t, h_vals[0])) {
+      res->fire_t = t;
+      stop = PCGPU_STOP_PERIODIC;
+      break;
+    }
+  }
+  h->buf[kField] = cur;
+  h->buf[kNext] = nxt;
+  h->buf[kIterT] = spare;
+  h->from_state(cur, field);
+  CK(cudaStreamSynchronize(h->stream));
+  res->t = t;
+  res->reason = stop;
+  if (!h->runner) h->runner = new pcgpu_runner_state();
+  h->runner->detector_rows = detect ? det.rs.rows : std::vector<std::vector<double>>{};
+  h->runner->samples = cfg->detector_samples_per_period;
+  res->detector_periods = static_cast<int32_t>(h->runner->detector_rows.size());
+  GUARD_END(h)
+  return PCGPU_OK;
+}
+
+int pcgpu_evolve_host(pcgpu_stepper* h, double* field_host, const pcgpu_runner_cfg* cfg,
+                      pcgpu_step_cb on_step, pcgpu_snapshot_cb on_snapshot, void* user,
+                      pcgpu_evolve_result* res) {
+  if (!h || !field_host) return PCGPU_ERR_ARG;
+  // Trampolines: the step callback passes through, snapshots are copied to a
+  // host buffer first.
+  struct Ctx {
+    pcgpu_step_cb step;
+    pcgpu_snapshot_cb snap;
+    void* user;
+    std::vector<double> host;
+    size_t cells;
+    bool copy_failed = false;
+  } ctx{on_step, on_snapshot, user, {}, h->cells()};
+  auto step_tr = [](void* u, int64_t k, double t, double tau, const double* v) {
+    Ctx* c = static_cast<Ctx*>(u);
+    if (c->step) c->step(c->user, k, t, tau, v);
+  };
+  auto snap_tr = [](void* u, int32_t kind, double t, const double* fdev) {
+    Ctx* c = static_cast<Ctx*>(u);
+    if (!c->snap) return;
+    c->host.resize(c->cells);
+    if (cudaMemcpy(c->host.data(), fdev, sizeof(double) * c->cells, cudaMemcpyDeviceToHost) !=
+        cudaSuccess) {
+      c->copy_failed = true;
+      return;
+    }
+    c->snap(c->user, kind, t, c->host.data());
+  };
+  double* dev = nullptr;
+  GUARD_BEGIN
+  CK(cudaMalloc(&dev, sizeof(double) * h->cells()));
+  GUARD_END(h)
+  int rc = PCGPU_OK;
+  if (cudaMemcpy(dev, field_host, sizeof(double) * h->cells(), cudaMemcpyHostToDevice) !=
+      cudaSuccess)
+    rc = h->fail(PCGPU_ERR_CUDA, "evolve: field copy failed");
+  if (rc == PCGPU_OK) rc = pcgpu_evolve(h, dev, cfg, step_tr, snap_tr, &ctx, res);
+  if (rc == PCGPU_OK && ctx.copy_failed)
+    rc = h->fail(PCGPU_ERR_CUDA, "evolve: snapshot copy failed");
+  if (rc == PCGPU_OK &&
+      cudaMemcpy(field_host, dev, sizeof(double) * h->cells(), cudaMemcpyDeviceToHost) !=
+          cudaSuccess)
+    rc = h->fail(PCGPU_ERR_CUDA, "evolve: field copy failed");
+  cudaFree(dev);
+  return rc;
+}
+
+int pcgpu_detector_periods(const pcgpu_stepper* h, double* rows, int32_t max_rows) {
+  if (!h || !rows) return PCGPU_ERR_ARG;
+  if (!h->runner) return PCGPU_OK;
+  const auto& R = h->runner->detector_rows;
+  for (size_t k = 0; k < R.size() && static_cast<int32_t>(k) < max_rows; ++k)
+    std::copy(R[k].begin(), R[k].end(), rows + k * h->runner->samples);
   return PCGPU_OK;
 }
 

@@ -312,6 +312,12 @@ class AdiStepper:
     def launch_count(self) -> int:
         return int(self._lib.pcgpu_launch_count(self._h))
 
+    def evolve(self, timing, initial, t_end: float, cfg):
+        """pulsecell::evolve (runner.cpp:97-190) with the field resident on the
+        device; see paper_1912_03744_b200.runner.evolve."""
+        from .runner import evolve
+        return evolve(self, timing, initial, t_end, cfg)
+
     def describe(self) -> str:
         """The kernel variants the library selected for this problem."""
         buf = C.create_string_buffer(256)

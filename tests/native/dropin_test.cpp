@@ -7,6 +7,7 @@
 #include <cstring>
 
 #include "pulsecell/parallel.hpp"
+#include "pulsecell/runner.hpp"
 #include "pulsecell/solver.hpp"
 #include "pulsecell_gpu/adi_stepper.hpp"
 
@@ -87,7 +88,45 @@ int main() {
   } catch (const TauFloorError&) {
     threw = true;
   }
+  // evolve: the reference's runner on the CPU stepper vs pulsecell::gpu::evolve
+  RunnerConfig rc;
+  rc.t_end = 0.05;
+  rc.probes = {ProbeSpec{0.2e-3, 5e-3}, ProbeSpec{1.2e-3, 12e-3}};
+  rc.snapshot_times = {0.0, 0.011, 0.03};
+  rc.detector.samples_per_period = 8;
+  SolverConfig c2 = cfg;
+  c2.tau_transient_divisor = 100;
+  c2.tau_source_divisor = 100;
+  pulsecell::AdiStepper cpu2(grid, layers, src, timing, c2, pool);
+  pulsecell::gpu::AdiStepper gpu2(grid, layers, src, timing, c2, {0, true});
+  const EvolutionResult ec = evolve(cpu2, timing, make_field(grid, cfg.T0), rc.t_end, rc);
+  const EvolutionResult eg = pulsecell::gpu::evolve(gpu2, timing, make_field(grid, cfg.T0),
+                                                    rc.t_end, rc);
+  int ebad = 0;
+  if (ec.steps != eg.steps || ec.t != eg.t || ec.reason != eg.reason ||
+      ec.trace.size() != eg.trace.size() || ec.at_times.size() != eg.at_times.size() ||
+      ec.post_off.has_value() != eg.post_off.has_value())
+    ++ebad;
+  for (size_t k = 0; ebad == 0 && k < ec.trace.size(); ++k)
+    if (ec.trace[k].t != eg.trace[k].t || ec.trace[k].tau != eg.trace[k].tau ||
+        ec.trace[k].values != eg.trace[k].values)
+      ++ebad;
+  auto same = [&](const Array2& a, const Array2& b) {
+    for (Index i = 0; i < grid.nr(); ++i)
+      for (Index j = 0; j < grid.col_extent(i); ++j)
+        if (std::memcmp(&a(i, j), &b(i, j), sizeof(Real)) != 0) return false;
+    return true;
+  };
+  for (size_t k = 0; ebad == 0 && k < ec.at_times.size(); ++k)
+    if (ec.at_times[k].t != eg.at_times[k].t || !same(ec.at_times[k].field, eg.at_times[k].field))
+      ++ebad;
+  if (ebad == 0 && ec.post_off && (ec.post_off->t != eg.post_off->t ||
+                                   !same(ec.post_off->field, eg.post_off->field)))
+    ++ebad;
+  if (ebad == 0 && !same(ec.field, eg.field)) ++ebad;
   std::printf("dropin: steps with mismatching results %d, masked cells differing %ld, "
-              "TauFloorError mapped %s\n", bad, static_cast<long>(diff), threw ? "yes" : "no");
-  return (bad == 0 && diff == 0 && threw) ? 0 : 1;
+              "TauFloorError mapped %s, evolve (%ld steps, %zu snapshots) %s\n", bad,
+              static_cast<long>(diff), threw ? "yes" : "no", ec.steps, ec.at_times.size(),
+              ebad ? "DIFFERS" : "identical");
+  return (bad == 0 && diff == 0 && threw && ebad == 0) ? 0 : 1;
 }

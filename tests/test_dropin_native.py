@@ -18,3 +18,4 @@ def test_cpp_dropin_bitwise_vs_reference():
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "masked cells differing 0" in r.stdout
+    assert "evolve" in r.stdout and "identical" in r.stdout
