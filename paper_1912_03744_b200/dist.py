@@ -56,6 +56,19 @@ def share_unique_id(rank: int, device=None) -> bytes:
     return bytes(t.cpu().numpy().tobytes())
 
 
+def allgather_bytes(mine: bytes) -> bytes:
+    """Every rank's equal-length byte block, concatenated in rank order
+    (torch.distributed all_gather; CUDA tensors under NCCL, CPU under gloo)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.frombuffer(bytearray(mine), dtype=torch.uint8)
+    dev = f"cuda:{torch.cuda.current_device()}" if dist.get_backend() == "nccl" else "cpu"
+    parts = [torch.zeros(len(mine), dtype=torch.uint8, device=dev)
+             for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, t.to(dev))
+    return b"".join(bytes(p.cpu().numpy().tobytes()) for p in parts)
+
+
 class PartitionedAdi:
     """z-slab / r-slab partitioned AdiStepper.
 
@@ -131,17 +144,9 @@ class PartitionedAdi:
         """Exact mode, one process per GPU: map every rank's slabs into this
         process (CUDA IPC handles all-gathered over torch.distributed), so the
         fused K3/K4 passes store straight into the peers over NVLink."""
-        import torch
-        import torch.distributed as dist
         mine = (C.c_uint8 * N.DIST_IPC_BYTES)()
         self._check(self._lib.pcgpu_dist_ipc_export(self._h, mine))
-        t = torch.frombuffer(bytearray(bytes(mine)), dtype=torch.uint8)
-        world = dist.get_world_size()
-        dev = f"cuda:{torch.cuda.current_device()}" if dist.get_backend() == "nccl" else "cpu"
-        parts = [torch.zeros(N.DIST_IPC_BYTES, dtype=torch.uint8, device=dev)
-                 for _ in range(world)]
-        dist.all_gather(parts, t.to(dev))
-        blob = b"".join(bytes(p.cpu().numpy().tobytes()) for p in parts)
+        blob = allgather_bytes(bytes(mine))
         allh = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
         self._check(self._lib.pcgpu_dist_ipc_import(self._h, allh))
 

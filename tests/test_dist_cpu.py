@@ -37,6 +37,9 @@ def _worker(rank, world, port, q):
                 gathered = [torch.zeros_like(t) for _ in range(world)]
                 dist.all_gather(gathered, t)
                 out[(name, nr)] = [x.tolist() for x in gathered]
+        # the peer-transport handle exchange: equal blocks, rank order
+        blob = pdist.allgather_bytes(bytes([rank + 1]) * 256)
+        out["blob"] = blob
         uid = pdist.share_unique_id(rank)
         ids = [None] * world
         dist.all_gather_object(ids, uid)
@@ -60,8 +63,10 @@ def test_gloo_world2_plan_and_unique_id():
         assert p.exitcode == 0
     r0 = results[0]
     assert len(set(r0["ids"])) == 1 and len(r0["ids"][0]) == 128
+    expect = bytes([1]) * 256 + bytes([2]) * 256
+    assert results[0]["blob"] == expect and results[1]["blob"] == expect
     for key, plans in r0.items():
-        if key == "ids":
+        if key in ("ids", "blob"):
             continue
         assert plans[0] == plans[1], key  # identical plan on every rank
         name, nr = key
