@@ -244,6 +244,30 @@ def test_field_source_half_steps_bitwise(cuda):
     assert np.array_equal(ng[g.mask()], no[g.mask()])
 
 
+@pytest.mark.parametrize("kind", ["exact-lean", "exact-x"])
+def test_field_source_exact_lookups_half_steps_bitwise(cuda, kind, monkeypatch):
+    """A bound per-cell source on the power-law tables: the ws kernels' aux
+    staging with both exact lookup variants, odd and even slab widths."""
+    if kind == "exact-x":
+        monkeypatch.setenv("PCGPU_NO_EXACTLEAN", "1")
+    case = configs.scaled(configs.cfg4(), [44, 5, 13, 3], 128, 87)
+    case.source_kind = configs.SOURCE_FIELD
+    g = case.grid()
+    src = _Manufactured(g)
+    gpu = gpu_stepper(case, "exact", src)
+    assert gpu.describe().endswith(kind)
+    port = PortStepper(case)
+    f = configs.smooth_field(g, 10.0)
+    t, tau = 0.01, 1e-5
+    port.bind_power_field(src.power_field(g, t + 0.5 * tau))
+    ho, hg = make_field(g, 0.0), make_field(g, 0.0)
+    assert gpu.radial_half_step(f, t, tau, hg) == port.radial_half_step(f, t, tau, ho)
+    assert np.array_equal(hg[g.mask()], ho[g.mask()])
+    no, ng = make_field(g, 0.0), make_field(g, 0.0)
+    assert gpu.axial_half_step(ho, t, tau, ng) == port.axial_half_step(ho, t, tau, no)
+    assert np.array_equal(ng[g.mask()], no[g.mask()])
+
+
 @pytest.mark.parametrize("layout", [0, 1])
 def test_tridiag_batch_exact_bitwise(cuda, layout):
     import torch
