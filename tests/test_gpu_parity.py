@@ -469,10 +469,13 @@ def test_partitioned_exact_emulated_bitwise(cuda, name, nranks, steps, transport
     assert tm["allreduces"] > 0
 
 
-def test_partitioned_exact_halving_and_clamps_vs_oracle(cuda):
+@pytest.mark.parametrize("transport", ["peer", "nccl"])
+def test_partitioned_exact_halving_and_clamps_vs_oracle(cuda, transport, monkeypatch):
     """Partitioned exact run with tau halvings and clamp events, against the
     oracle (the reference's algorithm) directly."""
     from paper_1912_03744_b200.dist import PartitionedAdi
+    if transport == "nccl":
+        monkeypatch.setenv("PCGPU_DIST_TRANSPORT", "nccl")
     case = _cfg4s()
     g = case.grid()
     f = make_field(g, case.solver.T0)
