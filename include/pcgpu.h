@@ -295,6 +295,25 @@ int pcgpu_evolve_host(pcgpu_stepper* h, double* field_host, const pcgpu_runner_c
  * detector_samples_per_period values), into rows (capacity max_rows). */
 int pcgpu_detector_periods(const pcgpu_stepper* h, double* rows, int32_t max_rows);
 
+/* ---- Asynchronous snapshot writer --------------------------
+ * write_snapshot (snapshot_io.cpp:26-60) off the critical path: submitting a
+ * device field enqueues a device-to-device copy into one of `slots` slots on
+ * `stream` (stream-ordered after the kernels that produced it), a copy to
+ * pinned host memory on the writer's copy stream, and the formatting and
+ * file write on a writer thread. Formats: 0 CSV (masked cells, z-major,
+ * "%.17g"), 1 VTK legacy structured grid -- the reference's bytes. Submit
+ * blocks only while every slot is in flight. z_center: the grid's nz axial
+ * cell centres (Grid::z_center). */
+typedef struct pcgpu_writer pcgpu_writer;
+int pcgpu_writer_create(const pcgpu_desc* desc, const double* z_center, int32_t slots,
+                        pcgpu_writer** out);
+void pcgpu_writer_destroy(pcgpu_writer* w); /* finishes pending writes */
+int pcgpu_writer_submit(pcgpu_writer* w, const double* field_dev, void* stream,
+                        const char* path, int32_t format, const char* header);
+/* Waits for every submitted snapshot; written = files completed so far. */
+int pcgpu_writer_flush(pcgpu_writer* w, int64_t* written);
+const char* pcgpu_writer_last_error(const pcgpu_writer* w);
+
 /* ---- Partitioned stepper: one node of B200s ------------------
  * z-slabs (radial lines j) for the radial sweep, r-slabs (axial lines i) for
  * the axial sweep, all-to-all transposes between them, allreduce(max) of the

@@ -131,6 +131,11 @@ def _load_ref():
             ("pcref_step", C.c_int, [_vp, _vp, C.c_double, S]),
             ("pcref_run", C.c_int, [_vp, _vp, C.c_double, C.c_int32, S, R]),
             ("pcref_evolve", C.c_int, [_vp, _vp, C.POINTER(RefEvolveIO)]),
+            ("pcref_write_snapshot", C.c_int, [_vp, _vp, C.c_char_p, C.c_int32, C.c_char_p]),
+            ("pcref_write_trace", C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, C.c_char_p,
+                                            C.c_char_p]),
+            ("pcref_write_phase_trace", C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_double,
+                                                  C.c_char_p, C.c_char_p]),
             ("pcref_clamp_events", C.c_int, [_vp, C.POINTER(C.c_uint64)]),
             ("pcref_apply_lambda_r", C.c_double, [_vp, _vp, C.c_int64, C.c_int64]),
             ("pcref_apply_lambda_z", C.c_double, [_vp, _vp, C.c_int64, C.c_int64]),

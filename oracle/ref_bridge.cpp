@@ -17,6 +17,7 @@
 #include "pulsecell/materials.hpp"
 #include "pulsecell/parallel.hpp"
 #include "pulsecell/runner.hpp"
+#include "pulsecell/snapshot_io.hpp"
 #include "pulsecell/solver.hpp"
 #include "pulsecell/source.hpp"
 #include "pulsecell/tridiagonal.hpp"
@@ -317,6 +318,48 @@ int pcref_evolve(pcref* h, double* field, pcref_evolve_io* io) {
       for (int32_t q = 0; q < io->detector_samples_per_period; ++q)
         io->det_values[k * io->detector_samples_per_period + q] = r.detector_periods[k][q];
     if (r.reason == StopReason::TauFloor) h->error = r.error;
+  } catch (const std::exception& e) {
+    return h->fail(e);
+  }
+  return PCGPU_OK;
+}
+
+int pcref_write_snapshot(pcref* h, const double* field, const char* path, int32_t format,
+                         const char* header) {
+  try {
+    write_snapshot(*h->grid, to_array(h, field), path,
+                   format == 0 ? SnapshotFormat::Csv : SnapshotFormat::VtkStructured, header);
+  } catch (const std::exception& e) {
+    return h->fail(e);
+  }
+  return PCGPU_OK;
+}
+
+int pcref_write_trace(pcref* h, const double* t, const double* values, int64_t n,
+                      int32_t n_probes, const char* path, const char* header) {
+  try {
+    std::vector<TraceEntry> tr(static_cast<size_t>(n));
+    for (int64_t k = 0; k < n; ++k) {
+      tr[k].t = t[k];
+      tr[k].values.assign(values + k * n_probes, values + (k + 1) * n_probes);
+    }
+    write_trace(tr, static_cast<size_t>(n_probes), path, header);
+  } catch (const std::exception& e) {
+    return h->fail(e);
+  }
+  return PCGPU_OK;
+}
+
+int pcref_write_phase_trace(pcref* h, const double* rows, int32_t n_rows, int32_t samples,
+                            double t_per, const char* path, const char* header) {
+  try {
+    std::vector<Vector> p;
+    for (int32_t r = 0; r < n_rows; ++r) {
+      Vector v(samples);
+      for (int32_t q = 0; q < samples; ++q) v[q] = rows[r * samples + q];
+      p.push_back(v);
+    }
+    write_phase_trace(p, t_per, path, header);
   } catch (const std::exception& e) {
     return h->fail(e);
   }

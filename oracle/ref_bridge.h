@@ -99,6 +99,15 @@ typedef struct pcref_evolve_io {
 } pcref_evolve_io;
 int pcref_evolve(pcref* h, double* field, pcref_evolve_io* io);
 
+/* snapshot_io.cpp (the reference's writers): format 0 CSV, 1 VTK structured.
+ * Trace: n steps of (t, values[n_probes]); phase trace: rows x samples. */
+int pcref_write_snapshot(pcref* h, const double* field, const char* path, int32_t format,
+                         const char* header);
+int pcref_write_trace(pcref* h, const double* t, const double* values, int64_t n,
+                      int32_t n_probes, const char* path, const char* header);
+int pcref_write_phase_trace(pcref* h, const double* rows, int32_t n_rows, int32_t samples,
+                            double t_per, const char* path, const char* header);
+
 /* Operators and diagnostics (solver.cpp:53-119). */
 double pcref_apply_lambda_r(const pcref* h, const double* field, int64_t i, int64_t j);
 double pcref_apply_lambda_z(const pcref* h, const double* field, int64_t i, int64_t j);

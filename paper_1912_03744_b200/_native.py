@@ -90,6 +90,8 @@ EXPORTS = [
     "pcgpu_dist_timing", "pcgpu_dist_launch_count", "pcgpu_run_growth", "pcgpu_describe", "pcgpu_dist_transport",
     "pcgpu_dist_ipc_export", "pcgpu_dist_ipc_import", "pcgpu_evolve", "pcgpu_detector_periods",
     "pcgpu_evolve_host",
+    "pcgpu_writer_create", "pcgpu_writer_destroy", "pcgpu_writer_submit", "pcgpu_writer_flush",
+    "pcgpu_writer_last_error",
 ]
 
 _lib = None
@@ -142,6 +144,11 @@ def load():
         "pcgpu_evolve": (C.c_int, [vp, vp, vp, STEP_CB, SNAP_CB, vp, vp]),
         "pcgpu_detector_periods": (C.c_int, [vp, vp, C.c_int32]),
         "pcgpu_evolve_host": (C.c_int, [vp, vp, vp, STEP_CB, SNAP_CB, vp, vp]),
+        "pcgpu_writer_create": (C.c_int, [C.POINTER(Desc), vp, C.c_int32, C.POINTER(vp)]),
+        "pcgpu_writer_destroy": (None, [vp]),
+        "pcgpu_writer_submit": (C.c_int, [vp, vp, vp, C.c_char_p, C.c_int32, C.c_char_p]),
+        "pcgpu_writer_flush": (C.c_int, [vp, C.POINTER(C.c_int64)]),
+        "pcgpu_writer_last_error": (C.c_char_p, [vp]),
         "pcgpu_tridiag_batch": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, C.c_int64, C.c_int32,
                                           C.c_int32, vp, C.POINTER(C.c_int64)]),
         "pcgpu_nccl_unique_id": (C.c_int, [vp]),

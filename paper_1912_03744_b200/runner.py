@@ -77,7 +77,8 @@ class RunnerConfig:  # runner.hpp:93-103
 @dataclass
 class Snapshot:  # runner.hpp:106-109
     t: float
-    field: np.ndarray
+    field: Optional[np.ndarray]
+    path: Optional[str] = None  # set when the snapshot went to a SnapshotWriter instead
 
 
 @dataclass
@@ -134,10 +135,16 @@ class EvolveResultC(C.Structure):
 
 
 
-def evolve(stepper, timing, initial, t_end: float, cfg: RunnerConfig) -> EvolutionResult:
+def evolve(stepper, timing, initial, t_end: float, cfg: RunnerConfig, writer=None,
+           snapshot_file=None) -> EvolutionResult:
     """pulsecell::evolve (runner.cpp:97-190) on an AdiStepper of this package.
     `initial` is a torch CUDA field (column-major (nr, nz)); it is advanced in
-    place and returned as result.field."""
+    place and returned as result.field.
+
+    With a snapshot_io.SnapshotWriter and snapshot_file(kind, t, index) ->
+    (path, SnapshotFormat, header) or None, snapshots are written to files off
+    the critical path (the device field goes to the writer; no host copy on
+    the stepping thread) and the result's Snapshots carry the path."""
     import torch
     cfg.validate()
     grid = stepper.grid()
@@ -166,9 +173,18 @@ def evolve(stepper, timing, initial, t_end: float, cfg: RunnerConfig) -> Evoluti
         except BaseException as e:  # noqa: BLE001
             errors.append(e)
 
+    counts = [0, 0, 0]
+
     def on_snap(_u, kind, t, ptr):
         try:
-            snap = Snapshot(t, host_copy(ptr))
+            target = snapshot_file(kind, t, counts[kind]) if (writer and snapshot_file) else None
+            counts[kind] += 1
+            if target is not None:
+                path, fmt, header = target
+                writer.submit(ptr, path, fmt, header)
+                snap = Snapshot(t, None, path)
+            else:
+                snap = Snapshot(t, host_copy(ptr))
             if kind == N.SNAP_PRE_ON:
                 res.pre_on = snap
             elif kind == N.SNAP_POST_OFF:

@@ -312,11 +312,11 @@ class AdiStepper:
     def launch_count(self) -> int:
         return int(self._lib.pcgpu_launch_count(self._h))
 
-    def evolve(self, timing, initial, t_end: float, cfg):
+    def evolve(self, timing, initial, t_end: float, cfg, writer=None, snapshot_file=None):
         """pulsecell::evolve (runner.cpp:97-190) with the field resident on the
         device; see paper_1912_03744_b200.runner.evolve."""
         from .runner import evolve
-        return evolve(self, timing, initial, t_end, cfg)
+        return evolve(self, timing, initial, t_end, cfg, writer, snapshot_file)
 
     def describe(self) -> str:
         """The kernel variants the library selected for this problem."""
