@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define PCGPU_ABI_VERSION 1
+#define PCGPU_ABI_VERSION 2
 
 /* Status codes. Reference equivalents in brackets. */
 enum pcgpu_status {
@@ -122,6 +122,14 @@ typedef struct pcgpu_desc {
   /* Device options (not part of the reference schema). */
   int32_t mode;   /* pcgpu_mode */
   int32_t device; /* CUDA device ordinal */
+
+  /* Generalised stepped domain (beyond the reference's
+   * two-level Grid): when both are non-NULL they give the masked extent of
+   * every line -- non-increasing, consistent prefix masks (i < row_extent[j]
+   * iff j < col_extent[i]). NULL: the reference's rule from nr_core /
+   * nz_shared above. */
+  const int32_t* row_extent; /* [nz] cells of radial line j */
+  const int32_t* col_extent; /* [nr] cells of axial line i */
 } pcgpu_desc;
 
 /* HalfStepOutcome (solver.hpp:50-54). */

@@ -32,6 +32,7 @@ enum { P_CV = 0, P_LAMBDA = 1, P_CHI = 2 };
 struct oracle {
   pcgpu_desc d; /* scalars; array pointers below are owned copies */
   int nr, nz, nr_core, nz_shared;
+  int *row_ext, *col_ext; /* masked extents (generalised stepped domain) */
   int* layer;
   double *r_center, *gap_r, *width_z, *gap_z;
   omaterial* mats;
@@ -214,6 +215,15 @@ int oracle_create(const pcgpu_desc* d, oracle** out) {
   o->nr_core = d->nr_core;
   o->nz_shared = d->nz_shared;
   const int nr = o->nr, nz = o->nz;
+  /* The reference's two-level Grid (geometry.hpp:72-74), or the explicit
+   * extents of a generalised stepped domain (beyond the reference). */
+  o->row_ext = (int*)malloc(sizeof(int) * nz);
+  o->col_ext = (int*)malloc(sizeof(int) * nr);
+  for (int j = 0; j < nz; ++j)
+    o->row_ext[j] = d->row_extent ? d->row_extent[j] : (j < d->nz_shared ? nr : d->nr_core);
+  for (int i = 0; i < nr; ++i)
+    o->col_ext[i] = d->col_extent ? d->col_extent[i] : (i < d->nr_core ? nz : d->nz_shared);
+  o->d.row_extent = o->d.col_extent = NULL;
   o->layer = (int*)malloc(sizeof(int) * nr);
   for (int i = 0; i < nr; ++i) o->layer[i] = d->layer[i];
   o->r_center = dup_d(d->r_center, nr);
@@ -270,6 +280,7 @@ int oracle_create(const pcgpu_desc* d, oracle** out) {
 
 void oracle_destroy(oracle* o) {
   if (!o) return;
+  free(o->row_ext); free(o->col_ext);
   free(o->layer); free(o->r_center); free(o->gap_r); free(o->width_z); free(o->gap_z);
   for (int m = 0; m < o->d.n_layers; ++m)
     for (int p = 0; p < 3; ++p) { free(o->mats[m].prop[p].t); free(o->mats[m].prop[p].v); }
@@ -295,8 +306,8 @@ int oracle_clamp_events(const oracle* o, uint64_t* counts) {
   return PCGPU_OK;
 }
 
-static int row_extent(const oracle* o, int j) { return j < o->nz_shared ? o->nr : o->nr_core; }
-static int col_extent(const oracle* o, int i) { return i < o->nr_core ? o->nz : o->nz_shared; }
+static int row_extent(const oracle* o, int j) { return o->row_ext[j]; }
+static int col_extent(const oracle* o, int i) { return o->col_ext[i]; }
 /* geometry.hpp:92-94 */
 static double face_r_lo(const oracle* o, int i) {
   return i == 0 ? 0.0 : 0.5 * (o->r_center[i - 1] + o->r_center[i]);

@@ -282,13 +282,14 @@ class PortStepper(_Base):
         self._check(rc)
         return float(st.t_end), stats, [_result(res[k]) for k in range(int(st.steps))]
 
-    def __init__(self, case, source_kind=None):
+    def __init__(self, case, source_kind=None, explicit_extents=False):
         from paper_1912_03744_b200.source import FieldSource, JouleSource, NullSource
         self.lib = _load_port()
         grid = case.grid()
         kind = case.source_kind if source_kind is None else source_kind
         src = _source_for(case, grid, kind)
-        desc, self._keep = build_desc(grid, case.materials, src, case.timing, case.solver)
+        desc, self._keep = build_desc(grid, case.materials, src, case.timing, case.solver,
+                                      explicit_extents=explicit_extents)
         h = _vp()
         rc = self.lib.oracle_create(C.byref(desc), C.byref(h))
         if rc != N.OK:

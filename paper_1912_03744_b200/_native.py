@@ -13,7 +13,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libpcgpu.so")
 
-PCGPU_ABI_VERSION = 1
+PCGPU_ABI_VERSION = 2
 DIST_IPC_BYTES = 256
 
 # pcgpu_status
@@ -57,6 +57,7 @@ class Desc(C.Structure):
         ("halfpoint_rule", C.c_int32), ("range_policy", C.c_int32), ("all_neumann", C.c_int32),
         ("T0", C.c_double), ("t_ceiling", C.c_double),
         ("mode", C.c_int32), ("device", C.c_int32),
+        ("row_extent", C.POINTER(C.c_int32)), ("col_extent", C.POINTER(C.c_int32)),
     ]
 
 

@@ -112,6 +112,19 @@ def cfg4(periods: float = 10.0) -> Case:
                 t_end=periods * 1.0, notes="2-level staircase: core to 22 mm, shell to 15 mm")
 
 
+def cfg4_staircase(periods: float = 10.0, insulator_length: float = 0.022) -> Case:
+    """configs[4] on the generalised stepped domain (beyond the
+    reference's two-level Grid): r_max(z) = 1.45 mm below 15 mm and 1.1 mm
+    above (core and insulator to `insulator_length` ... 22 mm), the copper
+    core to 22 mm. insulator_length < 22 mm gives three axial levels. No
+    reference oracle exists for it; the C restatement (oracle/) is the checker."""
+    c = cfg4(periods)
+    d = replace(c.domain, layer_lengths=[0.022, insulator_length, 0.015, 0.015])
+    return replace(c, name="cfg4-staircase", domain=d,
+                   notes=f"staircase: core 22 mm, insulator {insulator_length * 1e3:g} mm, "
+                         "heater and coating 15 mm")
+
+
 def scaled(case: Case, nr_div, nz_core: int, nz_outer: Optional[int] = None,
            name: Optional[str] = None) -> Case:
     """Same physics on a smaller grid (parity tests at oracle-friendly sizes)."""

@@ -50,10 +50,10 @@ constexpr int SEG = NT * R;    // rows per CTA
 constexpr int kMaxCluster = 8; // portable cluster size -> lines up to 16384 rows
 
 __device__ __forceinline__ int row_extent(const DevProblem& P, int j) {
-  return j < P.nz_shared ? P.nr : P.nr_core;
+  return __ldg(P.row_ext + j);
 }
 __device__ __forceinline__ int col_extent(const DevProblem& P, int i) {
-  return i < P.nr_core ? P.nz : P.nz_shared;
+  return __ldg(P.col_ext + i);
 }
 
 __device__ __forceinline__ bool skip_iteration(const DevStatus* st, int it, double eps) {

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "../../include/pcgpu.h"
+#include "extents.h"
 #include "adi_kernels.h"
 
 using namespace pcgpu;
@@ -88,6 +89,10 @@ std::string validate(const pcgpu_desc* d) {
     return "stepper: invalid grid extents";
   if (!d->layer || !d->r_center || !d->gap_r || !d->width_z || !d->gap_z)
     return "stepper: null grid array";
+  {
+    const std::string e = check_extents(d);
+    if (!e.empty()) return e;
+  }
   if (d->n_layers < 1 || d->n_layers > kMaxLayers) return "stepper: one material required per layer";
   if (!d->materials) return "stepper: null material";
   for (int i = 0; i < d->nr; ++i)
@@ -163,6 +168,7 @@ struct pcgpu_runner_state {
 struct pcgpu_stepper {
   pcgpu_desc d{};
   pcgpu_runner_state* runner = nullptr;  // the last evolve's detector rows
+  std::vector<int> col_ext_host;         // masked extent of every axial line
   DevProblem P{};
   std::vector<void*> dev_allocs;
   cudaStream_t stream = nullptr;
@@ -666,6 +672,19 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
     P.nz = nz;
     P.nr_core = d->nr_core;
     P.nz_shared = d->nz_shared;
+    {
+      const std::vector<int> re = desc_row_extent(d), ce = desc_col_extent(d);
+      int* dre = nullptr;
+      int* dce = nullptr;
+      CK(cudaMalloc(&dre, sizeof(int) * re.size()));
+      CK(cudaMalloc(&dce, sizeof(int) * ce.size()));
+      allocs.push_back(dre);
+      allocs.push_back(dce);
+      CK(cudaMemcpy(dre, re.data(), sizeof(int) * re.size(), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(dce, ce.data(), sizeof(int) * ce.size(), cudaMemcpyHostToDevice));
+      P.row_ext = dre;
+      P.col_ext = dce;
+    }
     auto up = [&](const std::vector<double>& v) {
       double* p = dev_upload(v);
       allocs.push_back(p);
@@ -758,9 +777,13 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     const int nr = d->nr, nz = d->nz;
     h->tau_floor = d->tau_min > 0 ? d->tau_min : 1e-12 * d->t_per;  // solver.hpp:28-30
-    for (int i = 0; i < nr; ++i) h->active += (i < d->nr_core ? nz : d->nz_shared);
+    h->col_ext_host = desc_col_extent(d);
+    for (int i = 0; i < nr; ++i) h->active += h->col_ext_host[i];
+    (void)nz;
 
     build_dev_problem(d, h->P, h->dev_allocs);
+    // the caller's arrays are copied; the stepper keeps no pointer to them
+    h->d.row_extent = h->d.col_extent = nullptr;
 
     CK(cudaMalloc(&h->st, sizeof(DevStatus)));
     h->dev_allocs.push_back(h->st);
@@ -1196,8 +1219,7 @@ int pcgpu_evolve(pcgpu_stepper* h, double* field, const pcgpu_runner_cfg* cfg,
   std::vector<int> off(np);
   for (int k = 0; k < np; ++k) {
     const int i = cfg->probe_i[k], j = cfg->probe_j[k];
-    const bool in_mask = i >= 0 && i < d.nr && j >= 0 &&
-                         j < (i < d.nr_core ? d.nz : d.nz_shared);
+    const bool in_mask = i >= 0 && i < d.nr && j >= 0 && j < h->col_ext_host[i];
     if (!in_mask) return h->fail(PCGPU_ERR_CONFIG, "probe cell falls outside the domain");
     off[k] = h->fast() ? i * d.nz + j : j * d.nr + i;  // state layout
   }

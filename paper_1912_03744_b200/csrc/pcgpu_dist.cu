@@ -37,6 +37,7 @@
 
 #include "../../include/pcgpu.h"
 #include "adi_kernels.h"
+#include "extents.h"
 
 using namespace pcgpu;
 
@@ -726,11 +727,13 @@ int pcgpu_dist_create(const pcgpu_desc* d, int32_t rank, int32_t nranks, const v
     DCK(cudaEventCreate(&h->ev0));
     DCK(cudaEventCreate(&h->ev1));
     build_dev_problem(d, h->P, h->allocs);
+    h->d.row_extent = h->d.col_extent = nullptr;  // copied; no pointer kept
     const int nr = d->nr, nz = d->nz;
     h->tau_floor = d->tau_min > 0 ? d->tau_min : 1e-12 * d->t_per;
-    for (int i = 0; i < nr; ++i) h->active += (i < d->nr_core ? nz : d->nz_shared);
-    h->zb = split_lines(nz, nranks, [&](int j) { return j < d->nz_shared ? nr : d->nr_core; });
-    h->rb = split_lines(nr, nranks, [&](int i) { return i < d->nr_core ? nz : d->nz_shared; });
+    const std::vector<int> re = desc_row_extent(d), ce = desc_col_extent(d);
+    for (int i = 0; i < nr; ++i) h->active += ce[i];
+    h->zb = split_lines(nz, nranks, [&](int j) { return re[j]; });
+    h->rb = split_lines(nr, nranks, [&](int i) { return ce[i]; });
     std::vector<int> mine;
     if (h->local) {
       for (int p = 0; p < nranks; ++p) mine.push_back(p);
@@ -993,8 +996,9 @@ int64_t pcgpu_dist_launch_count(const pcgpu_dist* h) {
 int pcgpu_dist_plan(const pcgpu_desc* d, int32_t nranks, int32_t* zb, int32_t* rb) {
   if (!d || nranks < 1 || !zb || !rb) return PCGPU_ERR_ARG;
   const int nr = d->nr, nz = d->nz;
-  const auto z = split_lines(nz, nranks, [&](int j) { return j < d->nz_shared ? nr : d->nr_core; });
-  const auto r = split_lines(nr, nranks, [&](int i) { return i < d->nr_core ? nz : d->nz_shared; });
+  const std::vector<int> re = desc_row_extent(d), ce = desc_col_extent(d);
+  const auto z = split_lines(nz, nranks, [&](int j) { return re[j]; });
+  const auto r = split_lines(nr, nranks, [&](int i) { return ce[i]; });
   for (int p = 0; p <= nranks; ++p) {
     zb[p] = z[p];
     rb[p] = r[p];

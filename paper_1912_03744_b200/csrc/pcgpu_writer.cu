@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "../../include/pcgpu.h"
+#include "extents.h"
 
 namespace {
 
@@ -43,7 +44,8 @@ inline int fmt_real(char* buf, double v) { return std::snprintf(buf, 32, "%.17g"
 
 struct pcgpu_writer {
   int device = 0;
-  int nr = 0, nz = 0, nr_core = 0, nz_shared = 0;
+  int nr = 0, nz = 0;
+  std::vector<int> row_ext;
   std::vector<double> r_center, z_center;
   std::vector<int> layer;
   cudaStream_t copy_stream = nullptr;
@@ -57,8 +59,8 @@ struct pcgpu_writer {
   std::thread worker;
 
   size_t cells() const { return static_cast<size_t>(nr) * nz; }
-  int row_extent(int j) const { return j < nz_shared ? nr : nr_core; }
-  bool in_mask(int i, int j) const { return i < (j < nz_shared ? nr : nr_core); }
+  int row_extent(int j) const { return row_ext[j]; }
+  bool in_mask(int i, int j) const { return i < row_ext[j]; }
 
   void write(const Job& job, const double* f) {
     FILE* out = std::fopen(job.path.c_str(), "wb");
@@ -181,8 +183,7 @@ int pcgpu_writer_create(const pcgpu_desc* d, const double* z_center, int32_t slo
   w->device = d->device;
   w->nr = d->nr;
   w->nz = d->nz;
-  w->nr_core = d->nr_core;
-  w->nz_shared = d->nz_shared;
+  w->row_ext = pcgpu::desc_row_extent(d);
   w->r_center.assign(d->r_center, d->r_center + d->nr);
   w->z_center.assign(z_center, z_center + d->nz);
   w->layer.assign(d->layer, d->layer + d->nr);

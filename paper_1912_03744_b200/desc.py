@@ -39,7 +39,11 @@ def source_kind(source: SourceModel) -> int:
 
 
 def build_desc(grid: Grid, mats: LayerMaterials, source: SourceModel, timing: SourceSpec,
-               cfg, mode: int = N.MODE_EXACT, device: int = 0) -> Tuple[N.Desc, List[Any]]:
+               cfg, mode: int = N.MODE_EXACT, device: int = 0,
+               explicit_extents: bool = False) -> Tuple[N.Desc, List[Any]]:
+    """pcgpu_desc of a problem. The masked extents are passed as arrays for a
+    generalised stepped domain (or when explicit_extents is set); otherwise
+    the library derives them from nr_core / nz_shared like the reference."""
     keep: List[Any] = []
     layer = np.ascontiguousarray(grid.layer_arr, dtype=np.int32)
     arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in
@@ -74,4 +78,10 @@ def build_desc(grid: Grid, mats: LayerMaterials, source: SourceModel, timing: So
     d.all_neumann = 1 if cfg.all_neumann else 0
     d.T0, d.t_ceiling = cfg.T0, cfg.t_ceiling
     d.mode, d.device = int(mode), int(device)
+    if explicit_extents or not grid.domain().is_two_level():  # explicit extents
+        re = np.ascontiguousarray(grid.row_extents(), dtype=np.int32)
+        ce = np.ascontiguousarray(grid.col_extents(), dtype=np.int32)
+        keep += [re, ce]
+        d.row_extent = re.ctypes.data_as(C.POINTER(C.c_int32))
+        d.col_extent = ce.ctypes.data_as(C.POINTER(C.c_int32))
     return d, keep

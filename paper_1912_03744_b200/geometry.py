@@ -10,7 +10,7 @@ from __future__ import annotations
 
 import math
 from dataclasses import dataclass, field
-from typing import List
+from typing import List, Optional
 
 import numpy as np
 
@@ -33,6 +33,11 @@ class DomainSpec:
     outer_length: float = 0.0
     layer_materials: List[str] = field(default_factory=list)
     source_layer: int = 0
+    # Generalised stepped domain (beyond the reference): the
+    # axial length of every layer, non-increasing outward, the core's being
+    # core_length and the shortest outer_length. None: the reference's two
+    # levels (core_length for layer 0, outer_length for the others).
+    layer_lengths: Optional[List[float]] = None
 
     def validate(self) -> None:  # geometry.cpp:7-22
         if not self.layer_radii:
@@ -52,6 +57,25 @@ class DomainSpec:
             raise ConfigError("domain.layer_materials: needs one entry per layer")
         if self.source_layer < 0 or self.source_layer >= self.layer_count():
             raise ConfigError("domain.source_layer: out of range")
+        if self.layer_lengths is not None:
+            L = list(self.layer_lengths)
+            if len(L) != self.layer_count():
+                raise ConfigError("domain.layer_lengths: needs one entry per layer")
+            if any(not (b <= a) for a, b in zip(L, L[1:])):
+                raise ConfigError("domain.layer_lengths: must be non-increasing outward")
+            if L[0] != self.core_length or min(L) != self.outer_length:
+                raise ConfigError("domain.layer_lengths: must span outer_length .. core_length")
+
+    def lengths(self) -> List[float]:
+        """Axial length of every layer."""
+        if self.layer_lengths is not None:
+            return list(self.layer_lengths)
+        return [self.core_length] + [self.outer_length] * (self.layer_count() - 1)
+
+    def is_two_level(self) -> bool:
+        """True when the layer lengths are the reference's own rule."""
+        return self.layer_lengths is None or list(self.layer_lengths) == (
+            [self.core_length] + [self.outer_length] * (self.layer_count() - 1))
 
     def layer_count(self) -> int:
         return len(self.layer_radii)
@@ -120,13 +144,25 @@ class Grid:
         for q in range(spec.axial_divisions_outer):
             z_center.append((q + 0.5) * w)
             width_z.append(w)
-        if zmax > z0:
-            core_step = zmax / spec.axial_divisions_core
-            n_ext = max(1, _llround((zmax - z0) / core_step))
-            w = (zmax - z0) / n_ext
+        # Segments above the shared region: the reference's single extension
+        # [outer_length, core_length], or one per distinct layer length of a
+        # generalised domain, each sized with the core's axial step.
+        levels = sorted(set(domain.lengths()))
+        seg_end = [spec.axial_divisions_outer]  # z cells up to each level
+        core_step = zmax / spec.axial_divisions_core
+        for lo, hi in zip(levels, levels[1:]):
+            n_ext = max(1, _llround((hi - lo) / core_step))
+            w = (hi - lo) / n_ext
             for q in range(n_ext):
-                z_center.append(z0 + (q + 0.5) * w)
+                z_center.append(lo + (q + 0.5) * w)
                 width_z.append(w)
+            seg_end.append(len(z_center))
+        # masked extents: layer m spans the z cells below its length
+        lens = domain.lengths()
+        col_of_layer = [seg_end[levels.index(L)] for L in lens]
+        self._col_ext = np.array([col_of_layer[m] for m in layer], dtype=np.int32)
+        self._row_ext = np.array([int(np.sum(self._col_ext > j)) for j in range(len(z_center))],
+                                 dtype=np.int32)
         gap_r = [0.0] * (len(r_center) + 1)  # geometry.cpp:84-94
         gap_r[0], gap_r[-1] = width_r[0], width_r[-1]
         for i in range(1, len(r_center)):
@@ -182,10 +218,16 @@ class Grid:
         return float(self.gap_z_arr[j])
 
     def row_extent(self, j: int) -> int:
-        return self.nr() if j < self._nz_shared else self._nr_core
+        return int(self._row_ext[j])
 
     def col_extent(self, i: int) -> int:
-        return self.nz() if i < self._nr_core else self._nz_shared
+        return int(self._col_ext[i])
+
+    def row_extents(self) -> np.ndarray:
+        return self._row_ext
+
+    def col_extents(self) -> np.ndarray:
+        return self._col_ext
 
     def in_mask(self, i: int, j: int) -> bool:
         return 0 <= i < self.nr() and 0 <= j < self.col_extent(i)
@@ -213,8 +255,8 @@ class Grid:
     def mask(self) -> np.ndarray:
         """Boolean (nr, nz) array of in-mask cells."""
         m = np.zeros((self.nr(), self.nz()), dtype=bool)
-        m[: self._nr_core, :] = True
-        m[:, : self._nz_shared] = True
+        for i in range(self.nr()):
+            m[i, : self._col_ext[i]] = True
         return m
 
 
