@@ -24,13 +24,17 @@ void launch_radial_exact(const DevProblem& P, int it, double eps, double half_k,
                          const double* powT, double* outT, double* wT, double* xT,
                          DevStatus* st, cudaStream_t s);
 // K4 axial_fixed_rhs_pass (solver.cpp:259-284) from the T-layout half field:
-// kbarN, explN and halfN (transposed copy) in N layout.
+// kbarN, explN and halfN (transposed copy) in N layout. kbarN == nullptr: no
+// K-bar field (the c_V lookups are still made, for their clamp events / range
+// errors); the axial sweep then computes K-bar itself (kbar_on_the_fly).
 void launch_axial_rhs_exact(const DevProblem& P, double half_k, double pulse,
                             const double* halfT, const double* powN, double* kbarN,
                             double* explN, double* halfN, DevStatus* st, cudaStream_t s);
 // K2 one Picard iteration of the axial sweep (solver.cpp:286-332, :343-345),
-// N layout, thread per axial line.
-void launch_axial_exact(const DevProblem& P, int it, double eps, const double* TsN,
+// N layout, thread per axial line. kbarN == nullptr (only when
+// kbar_on_the_fly(P)): K-bar = rho * c_V(ThN) * half_k inside the sweep.
+bool kbar_on_the_fly(const DevProblem& P);
+void launch_axial_exact(const DevProblem& P, int it, double eps, double half_k, const double* TsN,
                         const double* ThN, const double* kbarN, const double* explN,
                         double* outN, double* wN, double* xN, DevStatus* st, cudaStream_t s);
 
@@ -41,8 +45,8 @@ void launch_radial_exact_slab(const DevProblem& P, int it, double eps, double ha
                               double pulse, int j0, int nj, const double* TsT, const double* TcT,
                               const double* explT, const double* powT, double* outT, double* wT,
                               double* xT, DevStatus* st, cudaStream_t s);
-void launch_axial_exact_slab(const DevProblem& P, int it, double eps, int i0, int ni,
-                             const double* TsN, const double* ThN, const double* kbarN,
+void launch_axial_exact_slab(const DevProblem& P, int it, double eps, double half_k, int i0,
+                             int ni, const double* TsN, const double* ThN, const double* kbarN,
                              const double* explN, double* outN, double* wN, double* xN,
                              DevStatus* st, cudaStream_t s);
 // K3 on an r-slab: explR = Lambda_z[TR]
@@ -51,7 +55,7 @@ void launch_expl_rslab_exact(const DevProblem& P, int i0, int ni, const double* 
 // K4 without K-bar on a z-slab: explZ = Lambda_r[halfZ] + X(halfZ)
 void launch_rhs_zslab_exact(const DevProblem& P, double pulse, int j0, int nj,
                             const double* halfZ, double* explZ, DevStatus* st, cudaStream_t s);
-// K-bar on an r-slab
+// K-bar on an r-slab (kbarR == nullptr: the clamp events / range errors only)
 void launch_kbar_rslab_exact(const DevProblem& P, double half_k, int i0, int ni,
                              const double* halfR, double* kbarR, DevStatus* st, cudaStream_t s);
 

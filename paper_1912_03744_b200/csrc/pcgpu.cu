@@ -377,11 +377,12 @@ struct pcgpu_stepper {
     auto dst_of = [&](int it) -> double* { return it % 2 == 1 ? out : buf[kIterT]; };
     int conv;
     if (!fast()) {
-      launch_axial_rhs_exact(P, hk, pulse, half, buf[kPowN], buf[kKbar], buf[kExpl], anchor, st,
-                             stream);
+      // exact lookups: the axial sweep computes K-bar from T_half (no K-bar field)
+      double* kbar = kbar_on_the_fly(P) ? nullptr : buf[kKbar];
+      launch_axial_rhs_exact(P, hk, pulse, half, buf[kPowN], kbar, buf[kExpl], anchor, st, stream);
       conv = picard(1, pred_axial, [&](int it) {
-        launch_axial_exact(P, it, d.epsilon, src_of(it), anchor, buf[kKbar], buf[kExpl],
-                           dst_of(it), buf[kW], buf[kX], st, stream);
+        launch_axial_exact(P, it, d.epsilon, hk, src_of(it), anchor, kbar, buf[kExpl], dst_of(it),
+                           buf[kW], buf[kX], st, stream);
       }, o);
     } else {
       launch_axial_rhs_fast(P, pulse, half, buf[kPowN], buf[kExpl], anchor, st, stream);
@@ -797,6 +798,7 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
     for (int b = 0; b < kNumBufs; ++b) {
       if ((b == kPowN || b == kPowT) && d->source_kind != PCGPU_SOURCE_FIELD) continue;
       if ((b == kW || b == kKbar) && d->mode == PCGPU_MODE_FAST) continue;  // exact-mode only
+      if (b == kKbar && kbar_on_the_fly(h->P)) continue;  // computed inside the axial sweep
       if (b == kStage) continue;  // lazily, by the *_host entry points
       double* p = nullptr;
       CK(cudaMalloc(&p, bytes));

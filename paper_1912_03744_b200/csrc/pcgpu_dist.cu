@@ -510,8 +510,12 @@ struct pcgpu_dist {
           double* const* d2[2] = {c.data(), e.data()};
           transpose_exact(true, 2, s2, d2);
         }
+        // K-bar: a field, or (exact lookups) computed by the axial sweep itself and
+        // only its c_V lookups' clamp events / range errors taken here
+        const bool fly = kbar_on_the_fly(P);
         for (RankState& R : ranks)
-          launch_kbar_rslab_exact(P, hk, R.i0, R.ni, R.rHalf, R.rKbar, R.st, stream);
+          launch_kbar_rslab_exact(P, hk, R.i0, R.ni, R.rHalf, fly ? nullptr : R.rKbar, R.st,
+                                  stream);
         reset_status(false);  // keep errors of the K4 passes
         auto rsrc = [&](RankState& R, int it) -> const double* {
           return it == 1 ? R.rHalf : (it % 2 == 0 ? R.rOut : R.rIter);
@@ -519,8 +523,9 @@ struct pcgpu_dist {
         auto rdst = [&](RankState& R, int it) -> double* { return it % 2 == 1 ? R.rOut : R.rIter; };
         const int aconv = picard(pred_a, [&](size_t lr, int it) {
           RankState& R = ranks[lr];
-          launch_axial_exact_slab(P, it, d.epsilon, R.i0, R.ni, rsrc(R, it), R.rHalf, R.rKbar,
-                                  R.rExpl, rdst(R, it), R.rW, R.rX, R.st, stream);
+          launch_axial_exact_slab(P, it, d.epsilon, hk, R.i0, R.ni, rsrc(R, it), R.rHalf,
+                                  fly ? nullptr : R.rKbar, R.rExpl, rdst(R, it), R.rW, R.rX,
+                                  R.st, stream);
         }, &r->axial, false);
         if (aconv < 0) return -aconv;
         *updates += static_cast<double>(active) * r->axial.iterations;
