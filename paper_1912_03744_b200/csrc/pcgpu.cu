@@ -627,6 +627,8 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
       for (int m = 0; m < d->n_layers; ++m) P.xe_rho[m] = P.mats[m].rho;
     }
     P.exact_ws = std::getenv("PCGPU_NO_EXACTWS") ? 0 : 1;
+    // test knob: every full tile of the line solvers takes the reciprocal redo path
+    P.rcp_redo = std::getenv("PCGPU_RCP_REDO") ? 1 : 0;
     std::vector<double> lt, lab;  // lean tables, uploaded below
     if (P.lean) {
       // property-grouped lean table: (prop, layer, k) -> {v[k-1], slope_k}

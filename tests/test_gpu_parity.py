@@ -69,6 +69,24 @@ def test_exact_cfg0_2000_steps_bitwise(cuda):
     assert max(r.radial.iterations for r in res_o) >= 2  # nonlinear Picard work happened
 
 
+def test_exact_rcp_redo_path_bitwise(cuda, monkeypatch):
+    """The line solvers' fallback for a flagged pivot (the tile redone with
+    __drcp_rn from the saved recurrence state), forced on every full tile."""
+    monkeypatch.setenv("PCGPU_RCP_REDO", "1")
+    case = configs.cfg0(200)
+    g = case.grid()
+    port = PortStepper(case)
+    fo = make_field(g, case.solver.T0)
+    te_o, _, res_o = port.run(fo, 0.0, case.steps)
+    gpu = gpu_stepper(case, "exact")
+    fg = to_dev(make_field(g, case.solver.T0))
+    te_g, _, res_g = gpu.run(fg, 0.0, case.steps, keep_results=True)
+    assert te_g == te_o
+    assert np.array_equal(_seq(res_g), _seq(res_o))
+    m = g.mask()
+    assert np.array_equal(to_host(fg)[m], fo[m])
+
+
 @pytest.mark.parametrize("rule", list(HalfPointRule))
 @pytest.mark.parametrize("api", ["device", "host"])
 def test_exact_half_steps_bitwise(cuda, rule, api):
