@@ -730,6 +730,16 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
     if (P.exact_lean) P.xe_tab = up(xe);
     P.source_kind = d->source_kind;
     P.source_layer = d->source_layer;
+    if (d->source_kind == PCGPU_SOURCE_JOULE) {  // chi_x2's constants
+      const DevMaterial& m = P.mats[P.source_layer];
+      P.chi_t0 = m.t_first[kChi];
+      P.chi_tK = m.t_last[kChi];
+      P.chi_vl = m.v_first[kChi];
+      P.chi_vh = m.v_last[kChi];
+      P.chi_dt = P.chi_tK - P.chi_t0;
+      P.chi_dv = P.chi_vh - P.chi_vl;
+      P.chi_rdt = m.rdt[kChi];
+    }
     P.amplitude = d->amplitude;
     P.halfpoint_rule = d->halfpoint_rule;
     P.range_policy = d->range_policy;
