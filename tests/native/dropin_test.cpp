@@ -5,11 +5,26 @@
 // reference headers), run on the GPU box by tests/test_dropin_native.py.
 #include <cstdio>
 #include <cstring>
+#include <filesystem>
+#include <unistd.h>
+#include <fstream>
+#include <sstream>
 
 #include "pulsecell/parallel.hpp"
 #include "pulsecell/runner.hpp"
+#include "pulsecell/snapshot_io.hpp"
 #include "pulsecell/solver.hpp"
 #include "pulsecell_gpu/adi_stepper.hpp"
+#include "pulsecell_gpu/cli_device.hpp"
+
+namespace {
+std::string slurp(const std::string& path) {
+  std::ifstream f(path, std::ios::binary);
+  std::stringstream ss;
+  ss << f.rdbuf();
+  return ss.str();
+}
+}  // namespace
 
 using namespace pulsecell;
 
@@ -124,9 +139,46 @@ int main() {
                                    !same(ec.post_off->field, eg.post_off->field)))
     ++ebad;
   if (ebad == 0 && !same(ec.field, eg.field)) ++ebad;
+  // simulate --device (cli_device.hpp): the files of cli.cpp's run_simulate,
+  // written by the reference's writers from the CPU evolve above and from
+  // gpu::simulate, must be byte-identical
+  namespace fs = std::filesystem;
+  const fs::path base = fs::temp_directory_path() / ("pcgpu_cli_" + std::to_string(::getpid()));
+  const std::string dc = (base / "cpu").string(), dg = (base / "gpu").string();
+  fs::create_directories(dc);
+  fs::create_directories(dg);
+  const std::string header = "# dropin cli test";
+  write_trace(ec.trace, rc.probes.size(), dc + "/trace.csv", header);
+  if (!ec.detector_periods.empty())
+    write_phase_trace(ec.detector_periods, timing.t_per, dc + "/trace_phases.csv", header);
+  auto outputs = [&](const Array2& f, const std::string& stem) {
+    write_snapshot(grid, f, stem + ".csv", SnapshotFormat::Csv, header);
+    write_snapshot(grid, f, stem + ".vtk", SnapshotFormat::VtkStructured, header);
+  };
+  if (ec.pre_on) outputs(ec.pre_on->field, dc + "/snapshot_pre_on");
+  if (ec.post_off) outputs(ec.post_off->field, dc + "/snapshot_post_off");
+  for (size_t k = 0; k < ec.at_times.size(); ++k)
+    outputs(ec.at_times[k].field, dc + "/snapshot_t" + std::to_string(k));
+  outputs(ec.field, dc + "/field_final");
+  pulsecell::gpu::simulate(grid, layers, src, timing, c2, rc, rc.t_end, dg, header, {0, true});
+  int files = 0, fbad = 0;
+  for (const auto& e : fs::directory_iterator(dc)) {
+    ++files;
+    const fs::path other = fs::path(dg) / e.path().filename();
+    if (!fs::exists(other) || slurp(e.path().string()) != slurp(other.string())) ++fbad;
+  }
+  for (const auto& e : fs::directory_iterator(dg))
+    if (!fs::exists(fs::path(dc) / e.path().filename())) ++fbad;
+  fs::remove_all(base);
+  // bench --device: the timing loop of bench.cpp on the GPU stepper
+  const BenchReport br = pulsecell::gpu::run_benchmark(grid, layers, src, timing, cfg, 3, {0, true});
+  const bool bench_ok = br.rows.size() == 1 && br.rows[0].wall_s > 0 && br.nr == grid.nr();
   std::printf("dropin: steps with mismatching results %d, masked cells differing %ld, "
-              "TauFloorError mapped %s, evolve (%ld steps, %zu snapshots) %s\n", bad,
+              "TauFloorError mapped %s, evolve (%ld steps, %zu snapshots) %s, "
+              "simulate --device files %d differing %d, bench --device %s\n", bad,
               static_cast<long>(diff), threw ? "yes" : "no", ec.steps, ec.at_times.size(),
-              ebad ? "DIFFERS" : "identical");
-  return (bad == 0 && diff == 0 && threw && ebad == 0) ? 0 : 1;
+              ebad ? "DIFFERS" : "identical", files, fbad, bench_ok ? "ok" : "FAILED");
+  return (bad == 0 && diff == 0 && threw && ebad == 0 && files > 0 && fbad == 0 && bench_ok)
+             ? 0
+             : 1;
 }
