@@ -339,6 +339,41 @@ def run_partitioned(args, case, rank, world, local, pg, grid_desc, metric):
     pg.all_reduce(tr, op=pg.ReduceOp.MAX)
     # every rank counts the whole grid's cell-updates (the norm is global)
     value = stats["cell_updates"] / (ms_max / 1e3)
+
+    # e2e through the partitioned stepper's host-field entry points: every
+    # step each rank copies its state lines (1/world of the field) in from
+    # pinned host memory and back out, over its own PCIe link
+    e2e = None
+    if not args.no_e2e and args.mode == "exact":
+        part.enable_timing(False)
+        host_t = torch.full((g.nz(), g.nr()), case.solver.T0, dtype=torch.float64).pin_memory()
+        hp = host_t.numpy().T  # (nr, nz) Fortran view of pinned memory
+        part.get_field_host(hp)
+        n_e2e = max(1, min(args.steps, 3))
+        te = t_end
+        part.set_field_host(hp)  # untimed first pass (page-in of the pinned buffer)
+        te, _, _ = part.run(te, 1)
+        part.get_field_host(hp)
+        pg.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        upd = 0.0
+        for _ in range(n_e2e):
+            part.set_field_host(hp)
+            te, st1, _ = part.run(te, 1)
+            part.get_field_host(hp)
+            upd += st1["cell_updates"]
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        pg.all_reduce(e_ms, op=pg.ReduceOp.MAX)
+        e2e = {"value": upd / (float(e_ms.item()) / 1e3), "unit": "cell-updates/s",
+               "h2d_bytes_per_step": g.nr() * g.nz() * 8, "d2h_bytes_per_step": g.nr() * g.nz() * 8,
+               "steps": n_e2e,
+               "api": "pcgpu_dist_set_field_host / run / get_field_host (C-ABI, host field; "
+                      "each rank moves its 1/N of the field)"}
     if rank == 0:
         z0, z1, r0, r1 = part.slabs()
         line = {
@@ -357,7 +392,7 @@ def run_partitioned(args, case, rank, world, local, pg, grid_desc, metric):
                           "fields_per_step": 4,
                           "bytes_per_rank_per_step":
                               4 * 8 * g.nr() * g.nz() // world * (world - 1) // world},
-            "clocks": clk.summary(), "gpu_launches": launches, "e2e": None,
+            "clocks": clk.summary(), "gpu_launches": launches, "e2e": e2e,
         }
         print(json.dumps(line))
 

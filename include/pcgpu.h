@@ -348,6 +348,13 @@ int pcgpu_dist_set_field(pcgpu_dist* h, const double* field_dev);
 /* Writes this process's lines into the full-size device field: the r-slab
  * columns (axial lines) in exact mode, the z-slab rows in fast mode. */
 int pcgpu_dist_get_field(pcgpu_dist* h, double* field_dev);
+/* Exact mode, host fields (nr x nz column-major, ideally pinned): copy only
+ * this process's state lines -- the r-slab columns (axial lines) -- in from /
+ * out to the full-size host field, so that each rank moves 1/nranks of the
+ * field over its own PCIe link. set_field_host also refreshes the z-slab copy
+ * (NCCL transpose) when the peer transport is off. */
+int pcgpu_dist_set_field_host(pcgpu_dist* h, const double* field_host);
+int pcgpu_dist_get_field_host(pcgpu_dist* h, double* field_host);
 /* Exact mode transport: 1 = peer stores from the fused slab passes (the
  * default for emulated ranks; after pcgpu_dist_ipc_import for processes),
  * 0 = NCCL all-to-all transposes. */

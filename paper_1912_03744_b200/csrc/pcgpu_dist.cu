@@ -900,6 +900,58 @@ int pcgpu_dist_get_field(pcgpu_dist* h, double* fieldN) {
   return PCGPU_OK;
 }
 
+int pcgpu_dist_set_field_host(pcgpu_dist* h, const double* host) {
+  if (!h->exact()) {
+    h->err = "pcgpu_dist_set_field_host: exact mode only";
+    return PCGPU_ERR_CONFIG;
+  }
+  try {
+    const int nr = h->d.nr;
+    std::vector<double*> a, b;
+    for (RankState& R : h->ranks) {
+      // r-slab N layout [j][i - i0] <- host columns i0 .. i0+ni-1
+      if (R.ni)
+        DCK(cudaMemcpy2DAsync(R.rTc, sizeof(double) * R.ni, host + R.i0, sizeof(double) * nr,
+                              sizeof(double) * R.ni, h->d.nz, cudaMemcpyHostToDevice,
+                              h->stream));
+      a.push_back(R.rTc);
+      b.push_back(R.zTc);
+    }
+    // the peer transport rebuilds the z-slab anchor from rTc in every attempt's
+    // fused K3; the NCCL transport keeps it, so refresh it like an acceptance
+    if (!h->peer) {
+      double* const* s1[1] = {a.data()};
+      double* const* d1[1] = {b.data()};
+      h->transpose_exact(false, 1, s1, d1);
+    }
+    DCK(cudaStreamSynchronize(h->stream));
+  } catch (const DistError& e) {
+    h->err = e.what;
+    return e.code;
+  }
+  return PCGPU_OK;
+}
+
+int pcgpu_dist_get_field_host(pcgpu_dist* h, double* host) {
+  if (!h->exact()) {
+    h->err = "pcgpu_dist_get_field_host: exact mode only";
+    return PCGPU_ERR_CONFIG;
+  }
+  try {
+    const int nr = h->d.nr;
+    for (RankState& R : h->ranks)
+      if (R.ni)
+        DCK(cudaMemcpy2DAsync(host + R.i0, sizeof(double) * nr, R.rTc, sizeof(double) * R.ni,
+                              sizeof(double) * R.ni, h->d.nz, cudaMemcpyDeviceToHost,
+                              h->stream));
+    DCK(cudaStreamSynchronize(h->stream));
+  } catch (const DistError& e) {
+    h->err = e.what;
+    return e.code;
+  }
+  return PCGPU_OK;
+}
+
 int pcgpu_dist_run(pcgpu_dist* h, double t0, int32_t nsteps, pcgpu_step_result* results,
                    pcgpu_run_stats* stats) {
   pcgpu_run_stats s{};

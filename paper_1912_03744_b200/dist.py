@@ -83,6 +83,7 @@ class PartitionedAdi:
         cfg.validate()
         timing.validate()
         self._grid = grid
+        self._nr, self._nz = grid.nr(), grid.nz()
         if mode not in ("exact", "fast"):
             raise ValueError("mode must be 'exact' or 'fast'")
         self.mode = mode
@@ -126,6 +127,25 @@ class PartitionedAdi:
 
     def get_field(self, field_dev) -> None:
         self._check(self._lib.pcgpu_dist_get_field(self._h, C.c_void_p(field_dev.data_ptr())))
+
+    @staticmethod
+    def _host_ptr(field, nr: int, nz: int, writable: bool):
+        a = field
+        if getattr(a, "shape", None) != (nr, nz) or a.dtype != "float64" or \
+                not a.flags["F_CONTIGUOUS"] or (writable and not a.flags["WRITEABLE"]):
+            raise ValueError("host field: a writable (nr, nz) float64 Fortran-ordered array")
+        return C.c_void_p(a.ctypes.data)
+
+    def set_field_host(self, field) -> None:
+        """Exact mode: this rank's state lines (r-slab columns) from a host
+        field ((nr, nz) float64, Fortran order; pinned for full PCIe speed)."""
+        nr, nz = self._nr, self._nz
+        self._check(self._lib.pcgpu_dist_set_field_host(self._h, self._host_ptr(field, nr, nz, False)))
+
+    def get_field_host(self, field) -> None:
+        """Exact mode: this rank's state lines into the host field."""
+        nr, nz = self._nr, self._nz
+        self._check(self._lib.pcgpu_dist_get_field_host(self._h, self._host_ptr(field, nr, nz, True)))
 
     def run(self, t0: float, nsteps: int, keep_results: bool = False):
         res = (N.StepResultC * nsteps)() if keep_results and nsteps > 0 else None

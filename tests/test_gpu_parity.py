@@ -488,6 +488,36 @@ def test_partitioned_exact_emulated_bitwise(cuda, name, nranks, steps, transport
 
 
 @pytest.mark.parametrize("transport", ["peer", "nccl"])
+def test_partitioned_exact_host_fields_bitwise(cuda, transport, monkeypatch):
+    """The host-field entry points of the partitioned stepper (each rank moves
+    only its state lines): step by step through host memory, as the bench's
+    multi-GPU e2e does, against the single-GPU host-field stepper."""
+    from paper_1912_03744_b200.dist import PartitionedAdi
+    if transport == "nccl":
+        monkeypatch.setenv("PCGPU_DIST_TRANSPORT", "nccl")
+    case = configs.cfg0()
+    g = case.grid()
+    src = configs.make_source(case, g)
+    single = gpu_stepper(case, "exact")
+    f1 = make_field(g, case.solver.T0)
+    part = PartitionedAdi(g, case.materials, src, case.timing, case.solver, device=0,
+                          emulate=3, mode="exact")
+    f2 = make_field(g, case.solver.T0)
+    t = 0.0
+    for _ in range(12):
+        r1 = single.step(f1, t)
+        part.set_field_host(f2)
+        _, _, r2 = part.run(t, 1, keep_results=True)
+        part.get_field_host(f2)
+        assert _seq([r1]).tolist() == _seq(r2).tolist()
+        t += r1.tau_used
+    m = g.mask()
+    assert np.array_equal(f2[m], f1[m])
+    with pytest.raises(ValueError):
+        part.get_field_host(np.zeros((g.nr(), g.nz())))  # C order
+
+
+@pytest.mark.parametrize("transport", ["peer", "nccl"])
 def test_partitioned_exact_halving_and_clamps_vs_oracle(cuda, transport, monkeypatch):
     """Partitioned exact run with tau halvings and clamp events, against the
     oracle (the reference's algorithm) directly."""
