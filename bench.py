@@ -263,6 +263,41 @@ def main():
                "h2d_bytes_per_step": nr * nz * 8, "d2h_bytes_per_step": nr * nz * 8,
                "steps": n_e2e, "api": "pcgpu_step_host (C-ABI, host field)"}
 
+    # Supplementary: a simulation through the package's device-resident runner
+    # (runner.evolve), the way a user runs many steps: the host
+    # field goes in once, every step hands the probe values back to the host,
+    # the final field comes back once; both copies are inside the timed region.
+    e2e_runner = None
+    if not args.no_e2e and world == 1:
+        from paper_1912_03744_b200.runner import ProbeSpec, RunnerConfig, evolve
+        k_run = max(3, args.steps)
+        rcfg = RunnerConfig(t_end=k_run * r.tau_used,
+                            probes=[ProbeSpec(0.5e-3, 5e-3), ProbeSpec(1.2e-3, 10e-3)],
+                            snapshot_pre_on=False, snapshot_post_off=False)
+        dev_field = torch.empty((nz, nr), dtype=torch.float64, device=f"cuda:{local}")
+        stepper.enable_kernel_timing(True)  # counts the Picard iterations that ran
+        torch.cuda.synchronize()
+        # copies and events on torch's stream (the pinned buffer must not be
+        # tied to the stepper's stream, which dies with the stepper); evolve
+        # blocks the host, so e1 is recorded after it
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dev_field.copy_(host_pinned, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        res = evolve(stepper, case.timing, dev_field.t(), rcfg.t_end, rcfg)
+        host_pinned.copy_(dev_field, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        kt = stepper.kernel_timing()
+        stepper.enable_kernel_timing(False)
+        r_ms = e0.elapsed_time(e1)
+        e2e_runner = {"value": active * (kt["radial_launches"] + kt["axial_launches"]) /
+                      (r_ms / 1e3), "unit": "cell-updates/s", "steps": res.steps,
+                      "h2d_bytes_total": nr * nz * 8, "d2h_bytes_total": nr * nz * 8,
+                      "d2h_bytes_per_step": 8 * len(rcfg.probes),
+                      "api": "runner.evolve (pcgpu_evolve: field resident, probes per step)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = run_reference_cpu(case, args.cpu_steps, 0, args.cpu_nz, os.cpu_count() or 1)
@@ -290,7 +325,8 @@ def main():
                          "ms_per_launch": dom_ms / max(dom_n, 1), "peak_kind": peak_kind,
                          "other_sweep_ms_per_launch": {k: v[0] / max(v[1], 1) for k, v in
                                                        sweeps.items()}},
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
+            "cpu_baseline": cpu, "e2e": e2e, "e2e_runner": e2e_runner, "clocks": clk.summary(),
+            "gpu_launches": launches,
         }
         print(json.dumps(line))
     if pg:
