@@ -320,6 +320,10 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_unit": "GB per launch (ncu dram__bytes_read+write)",
+                         # the same launch time against the DRAM bytes it really moves
+                         # (80 B per cell: the exact Thomas working set)
+                         "traffic_frac": (traffic / (dom_ms / max(dom_n, 1) / 1e3) / peak
+                                          if traffic and dom_n else None),
                          "kernel": f"{dom} Picard iteration ({args.mode})",
                          "bytes_per_launch": per_launch_bytes, "launches": dom_n,
                          "ms_per_launch": dom_ms / max(dom_n, 1), "peak_kind": peak_kind,
