@@ -69,6 +69,39 @@ def test_exact_cfg0_2000_steps_bitwise(cuda):
     assert max(r.radial.iterations for r in res_o) >= 2  # nonlinear Picard work happened
 
 
+@pytest.mark.parametrize("nr_div,nz", [
+    ([1, 1, 1, 1], 1),     # 4 x 1: a single row / single-cell lines
+    ([1, 1, 1, 1], 2),
+    ([2, 1, 1, 1], 3),     # odd line counts: no TMA (16-B row alignment)
+    ([9, 1, 4, 2], 33),    # one past a 32-line CTA, one past a 16-row tile
+    ([13, 1, 1, 1], 32),   # exactly one CTA of lines, exactly one radial tile
+    ([25, 2, 3, 2], 64),   # two axial tiles of 32 rows, 32 radial rows (two tiles)
+    ([40, 3, 9, 3], 97),
+])
+def test_exact_edge_grids_bitwise(cuda, nr_div, nz):
+    """Grids at and around the kernels' tile and CTA boundaries (and below
+    them) against the oracle: fields, tau / iteration / delta sequences."""
+    case = configs.scaled(configs.cfg0(12), nr_div, nz)
+    g = case.grid()
+    port = PortStepper(case)
+    f0 = configs.smooth_field(g, 30.0)
+    fo = f0.copy(order="F")
+    gpu = gpu_stepper(case, "exact")
+    fg = to_dev(f0.copy(order="F"))
+    try:
+        te_o, _, res_o = port.run(fo, 0.0, case.steps)
+    except OracleError as e:  # the reference gives up (tau floor): so must the GPU
+        with pytest.raises(TauFloorError):
+            gpu.run(fg, 0.0, case.steps)
+        assert "fell below floor" in str(e)
+        return
+    te_g, _, res_g = gpu.run(fg, 0.0, case.steps, keep_results=True)
+    assert te_g == te_o
+    assert np.array_equal(_seq(res_g), _seq(res_o))
+    m = g.mask()
+    assert np.array_equal(to_host(fg)[m], fo[m])
+
+
 def test_exact_rcp_redo_path_bitwise(cuda, monkeypatch):
     """The line solvers' fallback for a flagged pivot (the tile redone with
     __drcp_rn from the saved recurrence state), forced on every full tile."""
