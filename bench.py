@@ -379,6 +379,15 @@ def run_partitioned(args, case, rank, world, local, pg, grid_desc, metric):
     pg.all_reduce(tr, op=pg.ReduceOp.MAX)
     # every rank counts the whole grid's cell-updates (the norm is global)
     value = stats["cell_updates"] / (ms_max / 1e3)
+    # Roofline per GPU over the whole step (the partitioned stepper has no
+    # per-kernel timers): SURVEY 8(d)'s algorithmic bytes, 32 B per
+    # cell-update plus 16 B per cell and attempt for the explicit passes.
+    peak, peak_kind = load_peaks()
+    alg = 32.0 * stats["cell_updates"] + 16.0 * stats["attempt_cells"]
+    achieved = alg / world / (ms_max / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                "kernel": "whole partitioned step per GPU (algorithmic bytes / step time)"}
 
     # e2e through the partitioned stepper's host-field entry points: every
     # step each rank copies its state lines (1/world of the field) in from
@@ -432,7 +441,7 @@ def run_partitioned(args, case, rank, world, local, pg, grid_desc, metric):
                           "fields_per_step": 4,
                           "bytes_per_rank_per_step":
                               4 * 8 * g.nr() * g.nz() // world * (world - 1) // world},
-            "clocks": clk.summary(), "gpu_launches": launches, "e2e": e2e,
+            "roofline": roofline, "clocks": clk.summary(), "gpu_launches": launches, "e2e": e2e,
         }
         print(json.dumps(line))
 
