@@ -261,7 +261,8 @@ def main():
             pg.all_reduce(e_ms, op=pg.ReduceOp.MAX)
         e2e = {"value": upd * world / (float(e_ms.item()) / 1e3), "unit": "cell-updates/s",
                "h2d_bytes_per_step": nr * nz * 8, "d2h_bytes_per_step": nr * nz * 8,
-               "steps": n_e2e, "api": "pcgpu_step_host (C-ABI, host field)"}
+               "steps": n_e2e, "api": "pcgpu_step_host (C-ABI, host field)",
+               "copy_in_overlap": stepper.pipeline_stats()}
 
     # Supplementary: a simulation through the package's device-resident runner
     # (runner.evolve), the way a user runs many steps: the host

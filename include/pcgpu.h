@@ -202,6 +202,12 @@ int pcgpu_axial_half_step(pcgpu_stepper* h, const double* T_half, double t, doub
 int pcgpu_step(pcgpu_stepper* h, double* field, double t, pcgpu_step_result* result);
 /* Host-memory variants (H2D copy, step, D2H copy). */
 int pcgpu_step_host(pcgpu_stepper* h, double* field_host, double t, pcgpu_step_result* result);
+/* pcgpu_step_host copies the field in as row blocks overlapped with K3 and the
+ * first radial Picard iterations (exact mode, nz >= 2048 or
+ * $PCGPU_PIPELINE_MIN_NZ; off with $PCGPU_NO_PIPELINE). Counts of the steps
+ * that took that path and of those whose radial half-step had to be redone
+ * on the ordinary path (iteration count not as predicted). */
+int pcgpu_pipeline_stats(const pcgpu_stepper* h, int64_t* steps, int64_t* fallbacks);
 int pcgpu_radial_half_step_host(pcgpu_stepper* h, const double* T_cur_host, double t,
                                 double tau, double* out_host, pcgpu_outcome* outcome);
 int pcgpu_axial_half_step_host(pcgpu_stepper* h, const double* T_half_host, double t,

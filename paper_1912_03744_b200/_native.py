@@ -88,6 +88,7 @@ EXPORTS = [
     "pcgpu_tridiag_batch", "pcgpu_nccl_unique_id", "pcgpu_dist_create", "pcgpu_dist_destroy",
     "pcgpu_dist_last_error", "pcgpu_dist_plan", "pcgpu_dist_slabs", "pcgpu_dist_set_field",
     "pcgpu_dist_get_field", "pcgpu_dist_set_field_host", "pcgpu_dist_get_field_host",
+    "pcgpu_pipeline_stats",
     "pcgpu_dist_run", "pcgpu_dist_stream", "pcgpu_dist_enable_timing",
     "pcgpu_dist_timing", "pcgpu_dist_launch_count", "pcgpu_run_growth", "pcgpu_describe", "pcgpu_dist_transport",
     "pcgpu_dist_ipc_export", "pcgpu_dist_ipc_import", "pcgpu_evolve", "pcgpu_detector_periods",
@@ -164,6 +165,7 @@ def load():
         "pcgpu_dist_set_field": (C.c_int, [vp, vp]),
         "pcgpu_dist_get_field": (C.c_int, [vp, vp]),
         "pcgpu_dist_set_field_host": (C.c_int, [vp, vp]),
+        "pcgpu_pipeline_stats": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
         "pcgpu_dist_get_field_host": (C.c_int, [vp, vp]),
         "pcgpu_dist_run": (C.c_int, [vp, C.c_double, C.c_int32, C.POINTER(StepResultC),
                                      C.POINTER(RunStats)]),

@@ -41,10 +41,18 @@ void launch_axial_exact(const DevProblem& P, int it, double eps, double half_k, 
 // ---- partitioned (multi-GPU) slabs, exact mode (adi_exact.cu) ----
 // z-slab: radial lines j0..j0+nj-1, T layout [i][j-j0] (ld nj);
 // r-slab: axial lines i0..i0+ni-1, N layout [j][i-i0] (ld ni).
+// K3 over the row tiles covering [j_begin, j_end) (multiples of 64 rows except
+// at nz): the exact t3 kernel, for a field that arrives in row blocks.
+constexpr int kK3RowTile = 64;
+void launch_explicit_axial_exact_rows(const DevProblem& P, const double* srcN, double* explT,
+                                      double* srcT, DevStatus* st, int j_begin, int j_end,
+                                      cudaStream_t s);
+// ld: row stride of the line arrays (0: dense slab, ld = nj); the arrays may
+// then be a line range of a wider field (pointers offset to its first line).
 void launch_radial_exact_slab(const DevProblem& P, int it, double eps, double half_k,
                               double pulse, int j0, int nj, const double* TsT, const double* TcT,
                               const double* explT, const double* powT, double* outT, double* wT,
-                              double* xT, DevStatus* st, cudaStream_t s);
+                              double* xT, DevStatus* st, cudaStream_t s, long long ld = 0);
 void launch_axial_exact_slab(const DevProblem& P, int it, double eps, double half_k, int i0,
                              int ni, const double* TsN, const double* ThN, const double* kbarN,
                              const double* explN, double* outN, double* wN, double* xN,

@@ -132,6 +132,20 @@ std::string validate(const pcgpu_desc* d) {
   return "";
 }
 
+// dst[L] += sum of the first nslots counter rows (stride `stride`), L < n
+__global__ void k_add_counters(unsigned long long* dst, const unsigned long long* slots, int n,
+                               int stride, int nslots) {
+  const int L = threadIdx.x;
+  if (L >= n) return;
+  unsigned long long sum = 0;
+  for (int k = 0; k < nslots; ++k) sum += slots[static_cast<size_t>(k) * stride + L];
+  dst[L] += sum;
+}
+void launch_add_counters(unsigned long long* dst, const unsigned long long* slots, int n,
+                         int stride, int nslots, cudaStream_t s) {
+  k_add_counters<<<1, 32, 0, s>>>(dst, slots, n, stride, nslots);
+}
+
 template <typename T>
 T* dev_upload(const std::vector<T>& v) {
   T* p = nullptr;
@@ -180,6 +194,7 @@ struct pcgpu_stepper {
   std::string err;
   int64_t err_line = -1;
   int pred_radial = 1, pred_axial = 1;
+  bool pred_stable = false;  // the last two radial half-steps took the same iterations
   bool power_bound = false;
   // kernel timing
   bool timing = false;
@@ -190,10 +205,39 @@ struct pcgpu_stepper {
   double radial_ms = 0, axial_ms = 0;
   int64_t radial_launches = 0, axial_launches = 0;
   unsigned long long launches0 = 0;
+  // host-field steps with the copy-in pipelined into the radial sweep
+  // (radial_pipelined): lazily allocated
+  static constexpr int kPipeChunks = 8, kPipeMaxIter = 16;
+  cudaStream_t copy_stream = nullptr;
+  cudaStream_t chunk_stream[kPipeChunks] = {};
+  cudaEvent_t pipe_ev[kPipeChunks + 1] = {};
+  cudaEvent_t chunk_done[kPipeChunks] = {};
+  // [(kPipeMaxIter + 1) * kPipeChunks]: per row block, K3 (k = 0) then one
+  // status per iteration k -- index k * kPipeChunks + c
+  DevStatus* st_pipe = nullptr;
+  DevStatus* st_pipe_host = nullptr;  // pinned mirror
+  unsigned long long* clamp_pipe = nullptr;  // [kPipeMaxIter + 1][kMaxLayers]
+  double* pipe_spare = nullptr;       // third rotating radial iterate (T)
+  const double* pipe_host = nullptr;  // set by pcgpu_step_host for its first attempt
+  int64_t pipe_steps = 0, pipe_fallbacks = 0;
 
   ~pcgpu_stepper() {
     delete runner;
     if (stream) cudaStreamSynchronize(stream);
+    if (copy_stream) {
+      cudaStreamSynchronize(copy_stream);
+      cudaStreamDestroy(copy_stream);
+    }
+    for (auto& cs : chunk_stream)
+      if (cs) {
+        cudaStreamSynchronize(cs);
+        cudaStreamDestroy(cs);
+      }
+    for (auto& e : pipe_ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : chunk_done)
+      if (e) cudaEventDestroy(e);
+    if (st_pipe_host) cudaFreeHost(st_pipe_host);
     for (auto& e : ev_pool) cudaEventDestroy(e);
     for (void* p : dev_allocs) cudaFree(p);
     if (st_host) cudaFreeHost(st_host);
@@ -314,6 +358,7 @@ struct pcgpu_stepper {
           o->converged = 1;
           o->iterations = it;
           o->last_delta = dl;
+          if (sweep == 0) pred_stable = it == pred;
           pred = it;
           collect_timing(sweep, it);
           return it;
@@ -358,6 +403,152 @@ struct pcgpu_stepper {
     }
     if (conv < 0) return -conv;
     if (conv > 0) *res = dst_of(conv);
+    return PCGPU_OK;
+  }
+
+  // ---- radial half-step with the host field arriving in row blocks ----------
+  // The first attempt of a host-field step (pcgpu_step_host, exact mode): the
+  // field is copied in as kPipeChunks row blocks on a copy stream, and K3 plus
+  // Picard iterations 1..K (K = predicted + 1) of the radial lines in each
+  // block run as soon as the block (and the next one, for K3's halo row) has
+  // arrived -- a radial line needs only its own row. Lines are independent;
+  // only the stopping rule couples them, so no iteration is skipped here:
+  // iteration k of every block writes its delta / error into its own status
+  // and its clamp events into its own counters. Afterwards the host applies
+  // the reference's sequence -- K3's error, then per iteration its error and
+  // the convergence test -- and keeps the counters of the iterations the
+  // reference runs. Iterates rotate over three buffers, so the converged one
+  // survives up to two speculative iterations; otherwise (and when iteration K
+  // has not converged) the half-step is redone from the complete field on the
+  // ordinary path. Same arithmetic, same bits.
+  bool pipe_ready() {
+    if (copy_stream) return true;
+    CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    for (auto& cs : chunk_stream) CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    for (auto& e : pipe_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : chunk_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    const size_t nst = static_cast<size_t>(kPipeMaxIter + 1) * kPipeChunks;
+    CK(cudaMalloc(&st_pipe, sizeof(DevStatus) * nst));
+    dev_allocs.push_back(st_pipe);
+    CK(cudaMallocHost(&st_pipe_host, sizeof(DevStatus) * nst));
+    CK(cudaMalloc(&clamp_pipe, sizeof(unsigned long long) * (kPipeMaxIter + 1) * kMaxLayers));
+    dev_allocs.push_back(clamp_pipe);
+    CK(cudaMalloc(&pipe_spare, sizeof(double) * cells()));
+    dev_allocs.push_back(pipe_spare);
+    return true;
+  }
+
+  // *fallback: redo the half-step on the ordinary path (the copy is complete).
+  int radial_pipelined(const double* host, double* f, double t, double tau, const double** res,
+                       pcgpu_outcome* o, bool* fallback) {
+    pipe_ready();
+    *fallback = false;
+    const int nr = d.nr, nz = d.nz;
+    // speculate one iteration beyond the prediction unless the last two radial
+    // half-steps converged at the same count (then the tail is one iteration
+    // shorter; a longer one falls back)
+    const int K = std::min(std::min(d.max_iter, pred_radial + (pred_stable ? 0 : 1)),
+                           kPipeMaxIter);
+    const double pulse = pulse_for(t, tau);
+    const double hk = 2.0 / tau;
+    // row blocks: multiples of K3's 64-row tiles
+    int jc[kPipeChunks + 1];
+    const int rows = (nz + kPipeChunks * kK3RowTile - 1) / (kPipeChunks * kK3RowTile) * kK3RowTile;
+    for (int c = 0; c <= kPipeChunks; ++c) jc[c] = std::min(c * rows, nz);
+    // the copy stream starts after everything queued so far (f may still be read)
+    CK(cudaEventRecord(pipe_ev[kPipeChunks], stream));
+    CK(cudaStreamWaitEvent(copy_stream, pipe_ev[kPipeChunks], 0));
+    for (int c = 0; c < kPipeChunks; ++c) {
+      const size_t off = static_cast<size_t>(jc[c]) * nr;
+      const size_t n = static_cast<size_t>(jc[c + 1] - jc[c]) * nr;
+      if (n) CK(cudaMemcpyAsync(f + off, host + off, sizeof(double) * n, cudaMemcpyHostToDevice,
+                                copy_stream));
+      CK(cudaEventRecord(pipe_ev[c], copy_stream));
+    }
+    // statuses (per row block and iteration) and clamp counters (per iteration)
+    const size_t nst = static_cast<size_t>(K + 1) * kPipeChunks;
+    for (size_t q = 0; q < nst; ++q) {
+      CK(cudaMemsetAsync(st_pipe[q].delta, 0, sizeof(st_pipe[q].delta), stream));
+      CK(cudaMemsetAsync(&st_pipe[q].err, 0xff, sizeof(st_pipe[q].err), stream));
+    }
+    CK(cudaMemsetAsync(clamp_pipe, 0, sizeof(unsigned long long) * (K + 1) * kMaxLayers, stream));
+    CK(cudaEventRecord(pipe_ev[kPipeChunks], stream));  // the resets are done
+    double* rot[3] = {buf[kHalfT], buf[kIterT], pipe_spare};
+    auto dst_of = [&](int k) { return rot[(k - 1) % 3]; };
+    auto src_of = [&](int k) -> const double* { return k == 1 ? buf[kTcT] : dst_of(k - 1); };
+    auto slot = [&](int k) {
+      DevProblem Q = P;
+      Q.clamp = clamp_pipe + static_cast<size_t>(k) * kMaxLayers;
+      return Q;
+    };
+    const DevProblem Q0 = slot(0);
+    const double* powT = buf[kPowT];
+    // each row block on its own stream: blocks run concurrently once arrived
+    // (one block's Picard iterations are bound by its lines' pivot chains)
+    for (int c = 0; c < kPipeChunks; ++c) {
+      cudaStream_t cs = chunk_stream[c];
+      const int j0 = jc[c], nj = jc[c + 1] - jc[c];
+      CK(cudaStreamWaitEvent(cs, pipe_ev[kPipeChunks], 0));
+      if (nj > 0) {
+        CK(cudaStreamWaitEvent(cs, pipe_ev[std::min(c + 1, kPipeChunks - 1)], 0));
+        CK(cudaStreamWaitEvent(cs, pipe_ev[c], 0));
+        launch_explicit_axial_exact_rows(Q0, f, buf[kExpl], buf[kTcT], &st_pipe[c], j0, j0 + nj,
+                                         cs);
+        for (int k = 1; k <= K; ++k) {
+          const DevProblem Qk = slot(k);
+          // eps < 0: no iteration is skipped (the stopping rule is applied below)
+          launch_radial_exact_slab(Qk, k, -1.0, hk, pulse, j0, nj, src_of(k) + j0,
+                                   buf[kTcT] + j0, buf[kExpl] + j0,
+                                   powT ? powT + j0 : nullptr, dst_of(k) + j0, buf[kW] + j0,
+                                   buf[kX] + j0, &st_pipe[k * kPipeChunks + c], cs, nz);
+        }
+      }
+      CK(cudaEventRecord(chunk_done[c], cs));
+      CK(cudaStreamWaitEvent(stream, chunk_done[c], 0));
+    }
+    CK(cudaMemcpyAsync(st_pipe_host, st_pipe, sizeof(DevStatus) * nst, cudaMemcpyDeviceToHost,
+                       stream));
+    CK(cudaStreamSynchronize(stream));
+    ++pipe_steps;
+    auto add_clamps = [&](int upto) {
+      launch_add_counters(P.clamp, clamp_pipe, d.n_layers, kMaxLayers, upto + 1, stream);
+    };
+    // status k combined over the row blocks: lowest failing line, max delta
+    auto err_of = [&](int k) {
+      unsigned long long e = kNoError;
+      for (int c = 0; c < kPipeChunks; ++c) e = std::min(e, st_pipe_host[k * kPipeChunks + c].err);
+      return e;
+    };
+    auto delta_of_k = [&](int k) {
+      unsigned long long m = 0;  // non-negative doubles: integer max == double max
+      for (int c = 0; c < kPipeChunks; ++c) m = std::max(m, st_pipe_host[k * kPipeChunks + c].delta[k]);
+      double v;
+      std::memcpy(&v, &m, sizeof v);
+      return v;
+    };
+    auto fail_with = [&](int k) {  // the reference stops at this kernel
+      st_host->err = err_of(k);
+      add_clamps(k);
+      return check_line_error();
+    };
+    if (err_of(0) != kNoError) return -fail_with(0);
+    for (int k = 1; k <= K; ++k) {
+      if (err_of(k) != kNoError) return -fail_with(k);
+      const double dl = delta_of_k(k);
+      if (dl < d.epsilon) {
+        if (K - k >= 3) break;  // the converged iterate was overwritten: redo
+        add_clamps(k);
+        o->converged = 1;
+        o->iterations = k;
+        o->last_delta = dl;
+        pred_stable = k == pred_radial;
+        pred_radial = k;
+        *res = dst_of(k);
+        return PCGPU_OK;
+      }
+    }
+    ++pipe_fallbacks;
+    *fallback = true;
     return PCGPU_OK;
   }
 
@@ -418,9 +609,21 @@ struct pcgpu_stepper {
            pcgpu_step_result* r, double* attempt_updates, double tau0 = -1.0) {
     double tau = tau0 > 0 ? tau0 : host_initial_tau(d, t);
     std::memset(r, 0, sizeof *r);
+    const double* host = pipe_host;  // first attempt only
+    pipe_host = nullptr;
     for (;;) {
       const double* half = nullptr;
-      int rc = radial(field, t, tau, &half, &r->radial);
+      int rc;
+      bool redo = true;
+      if (host) {
+        rc = radial_pipelined(host, const_cast<double*>(field), t, tau, &half, &r->radial, &redo);
+        host = nullptr;
+        if (rc < 0) return -rc;
+      }
+      if (redo) {
+        r->radial = pcgpu_outcome{};
+        rc = radial(field, t, tau, &half, &r->radial);
+      }
       if (rc) return rc;
       *attempt_updates += static_cast<double>(active) * r->radial.iterations;
       if (r->radial.converged) {
@@ -1055,11 +1258,35 @@ static void ensure_stage(pcgpu_stepper* h) {
   h->buf[kStage] = p;
 }
 
+int pcgpu_pipeline_stats(const pcgpu_stepper* h, int64_t* steps, int64_t* fallbacks) {
+  if (!h || !steps || !fallbacks) return PCGPU_ERR_ARG;
+  *steps = h->pipe_steps;
+  *fallbacks = h->pipe_fallbacks;
+  return PCGPU_OK;
+}
+
 int pcgpu_step_host(pcgpu_stepper* h, double* field_host, double t, pcgpu_step_result* r) {
   if (!h || !field_host) return PCGPU_ERR_ARG;
   GUARD_BEGIN
   ensure_stage(h);
   double* f = h->buf[kStage];
+  const bool no_pipe = std::getenv("PCGPU_NO_PIPELINE") != nullptr;
+  const char* mv = std::getenv("PCGPU_PIPELINE_MIN_NZ");  // tests: pipeline small grids
+  const int min_nz = mv ? std::atoi(mv) : 2048;
+  if (!h->fast() && h->P.exact_ws && !no_pipe && h->d.nz >= min_nz) {
+    // the copy-in overlaps K3 and the first radial iterations (radial_pipelined);
+    // the accepted buffer goes straight back to the host
+    const double* acc = nullptr;
+    double upd = 0;
+    h->pipe_host = field_host;
+    const int rc = h->step(f, t, h->buf[kNext], &acc, r, &upd);
+    h->pipe_host = nullptr;
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(field_host, acc, sizeof(double) * h->cells(), cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return PCGPU_OK;
+  }
   CK(cudaMemcpyAsync(f, field_host, sizeof(double) * h->cells(), cudaMemcpyHostToDevice,
                      h->stream));
   const int rc = pcgpu_step(h, f, t, r);

@@ -309,6 +309,13 @@ class AdiStepper:
         return {"radial_ms": rm.value, "radial_launches": rl.value, "axial_ms": am.value,
                 "axial_launches": al.value}
 
+    def pipeline_stats(self) -> dict:
+        """Host-field steps that overlapped the copy-in with the radial sweep,
+        and how many of them redid the radial half-step (pcgpu_pipeline_stats)."""
+        a, b = C.c_int64(), C.c_int64()
+        self._check(self._lib.pcgpu_pipeline_stats(self._h, C.byref(a), C.byref(b)))
+        return {"steps": a.value, "fallbacks": b.value}
+
     def launch_count(self) -> int:
         return int(self._lib.pcgpu_launch_count(self._h))
 

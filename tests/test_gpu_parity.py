@@ -696,3 +696,76 @@ def test_exact_x_strict_range_lowest_line(cuda, lookup_kind):
             getattr(gpu, half)(f, 0.0, 1e-4, make_field(g, 0.0))
         assert eg.value.cause is TableRangeError
         assert eg.value.line == eo.value.line
+
+
+# ---- host-field steps with the copy-in pipelined into the radial sweep ----
+def _host_steps(port, gpu, f, t0, n):
+    """n steps through pcgpu_step_host (gpu) and the oracle on copies of f."""
+    fo, fg = f.copy(order="F"), f.copy(order="F")
+    res_o, res_g, t = [], [], t0
+    for _ in range(n):
+        ro = port.step(fo, t)
+        rg = gpu.step(fg, t)
+        res_o.append(ro)
+        res_g.append(rg)
+        t += ro.tau_used
+    return fo, fg, res_o, res_g
+
+
+@pytest.mark.parametrize("name", ["cfg0_nz1024", "cfg4s", "coarse_halving"])
+def test_host_step_pipelined_bitwise(cuda, monkeypatch, name):
+    """pcgpu_step_host with the field copied in as row blocks while K3 and the
+    first radial iterations run on the blocks already there: bit-identical to
+    the oracle step by step (fields, tau / halvings / iterations / deltas),
+    including the steps whose iteration count changes (redo path)."""
+    monkeypatch.setenv("PCGPU_PIPELINE_MIN_NZ", "1")
+    if name == "cfg0_nz1024":
+        case, f0, t0, n = configs.scaled(configs.cfg0(), [69, 7, 21, 3], 1024), None, 0.0, 30
+    elif name == "cfg4s":
+        case, f0, t0, n = _cfg4s(), None, 0.0, 25
+    else:
+        case = configs.scaled(configs.cfg0(), [23, 3, 7, 2], 48)
+        case.solver.tau_source_divisor = 10.0
+        case.solver.max_iter = 6
+        f0, t0, n = None, 0.02, 25
+    g = case.grid()
+    f = make_field(g, case.solver.T0) if f0 is None else f0
+    port, gpu = PortStepper(case), gpu_stepper(case, "exact")
+    fo, fg, res_o, res_g = _host_steps(port, gpu, f, t0, n)
+    assert np.array_equal(_seq(res_g), _seq(res_o))
+    m = g.mask()
+    assert np.array_equal(fg[m], fo[m])
+    assert gpu.clamp_events() == port.clamp_events()
+    ps = gpu.pipeline_stats()
+    assert ps["steps"] == n
+    if name == "coarse_halving":
+        assert sum(r.halvings for r in res_o) > 0
+
+
+def test_host_step_pipelined_clamps_and_strict(cuda, monkeypatch):
+    """Clamp events counted only for the iterations the reference runs, and
+    the reference's first failing line under the strict range policy."""
+    monkeypatch.setenv("PCGPU_PIPELINE_MIN_NZ", "1")
+    case = _cfg4s()
+    g = case.grid()
+    f = make_field(g, case.solver.T0)
+    f[10:12, 20:23] = 3.9
+    f[46, 30:32] = 3.95
+    f[50:52, 5:7] = 3.95
+    port, gpu = PortStepper(case), gpu_stepper(case, "exact")
+    fo, fg, res_o, res_g = _host_steps(port, gpu, f, 0.0, 6)
+    assert np.array_equal(_seq(res_g), _seq(res_o))
+    assert np.array_equal(fg[g.mask()], fo[g.mask()])
+    assert gpu.clamp_events() == port.clamp_events() and sum(port.clamp_events()) > 0
+    case2 = _cfg4s()
+    case2.solver.range_policy = RangePolicy.Strict
+    f2 = make_field(g, case2.solver.T0)
+    f2[40, 70] = 500.0
+    f2[20, 12] = 1.0
+    port2, gpu2 = PortStepper(case2), gpu_stepper(case2, "exact")
+    with pytest.raises(OracleError) as eo:
+        port2.step(f2.copy(order="F"), 0.0)
+    with pytest.raises(LineError) as eg:
+        gpu2.step(f2.copy(order="F"), 0.0)
+    assert eg.value.line == eo.value.line
+    assert gpu2.pipeline_stats()["steps"] == 1
