@@ -337,6 +337,52 @@ def test_tridiag_batch_exact_bitwise(cuda, layout):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("n,batch", [(2, 1), (16, 32), (30, 33), (1024, 200), (1000, 97),
+                                     (7, 40)])
+def test_tridiag_batch_contiguous_fused_ragged(cuda, n, batch):
+    """The fused contiguous kernel (TMA tiles of 16 rows x 32 systems) on sizes
+    that are not multiples of its tiles, bit for bit against the C restatement
+    of thomas_solve_inplace and against the transpose path (exact = 3); odd n
+    takes the transpose path (no 16-B row stride for TMA)."""
+    import ctypes as C
+    import torch
+    from oracle.oracle import port_thomas_batch
+    from paper_1912_03744_b200 import _native as N
+    from paper_1912_03744_b200.tridiagonal import thomas_solve_batch
+    rng = np.random.default_rng(n * 1000 + batch)
+    a = -rng.random((batch, n))
+    c = -rng.random((batch, n))
+    a[:, 0] = 0.0
+    c[:, -1] = 0.0
+    b = 2.05 + np.abs(a) + np.abs(c)
+    d = rng.random((batch, n)) * 2 - 1
+    host = [np.ascontiguousarray(v).reshape(-1) for v in (a, b, c, d)]
+    dev = [torch.from_numpy(h).cuda() for h in host]
+    x = torch.empty_like(dev[3])
+    thomas_solve_batch(*dev, x, n, batch, 0, exact=True)
+    rc, xo, _ = port_thomas_batch(*host, n, batch, 0)
+    assert rc == 0
+    assert np.array_equal(x.cpu().numpy(), xo)
+    x3 = torch.empty_like(dev[3])
+    failed = C.c_int64(-1)
+    assert N.load().pcgpu_tridiag_batch(*(C.c_void_p(t.data_ptr()) for t in (*dev, x3)), n, batch,
+                                        0, 3, None, C.byref(failed)) == N.OK
+    assert torch.equal(x, x3)
+
+
+def test_tridiag_batch_zero_pivot_fused(cuda):
+    import torch
+    from paper_1912_03744_b200.tridiagonal import thomas_solve_batch
+    n, batch = 48, 70
+    b = torch.ones(n * batch, dtype=torch.float64, device="cuda")
+    b[65 * n + 17] = 0.0
+    b[40 * n + 47] = 0.0
+    z = torch.zeros_like(b)
+    with pytest.raises(LineError) as e:
+        thomas_solve_batch(z, b, z, torch.ones_like(b), torch.empty_like(b), n, batch, 0)
+    assert e.value.line == 40
+
+
 def test_tridiag_batch_zero_pivot(cuda):
     import torch
     from paper_1912_03744_b200.tridiagonal import thomas_solve_batch
