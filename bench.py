@@ -138,6 +138,9 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="run the partitioned (multi-GPU) stepper even at world size 1 "
+                         "(under torchrun: a 1-rank NCCL communicator; validation of that path)")
     args = ap.parse_args()
     rank, world, local = dist_env()
 
@@ -169,7 +172,7 @@ def main():
 
     torch.cuda.set_device(local)
     pg = None
-    if world > 1:
+    if world > 1 or args.partitioned:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         pg = dist
@@ -177,7 +180,7 @@ def main():
     g = case.grid()
     nr, nz = g.nr(), g.nz()
     active = g.active_cells()
-    if world > 1:
+    if world > 1 or args.partitioned:
         run_partitioned(args, case, rank, world, local, pg, grid_desc, metric)
         pg.destroy_process_group()
         return
