@@ -502,6 +502,33 @@ def test_fast_cluster_lines_vs_oracle(cuda, shape):
     assert err <= max(FIXED_TOL, 20.0 * floor)
 
 
+def test_exact_cfg3_full_size_vs_reference(cuda):
+    """configs[3] at its full BASELINE size (8192 x 16384, 134M cells): two
+    exact-mode steps bit for bit against the reference's own AdiStepper
+    (oracle/_ref, on all host cores; the C restatement if the reference library
+    is absent) -- fields, tau, iteration counts and last_delta."""
+    import torch
+    from oracle.oracle import RefStepper, ref_available
+    case = configs.cfg3()
+    g = case.grid()
+    steps = 2
+    cpu = (RefStepper(case, workers=os.cpu_count() or 1) if ref_available()
+           else PortStepper(case))
+    fo = make_field(g, case.solver.T0)
+    te_o, _, res_o = cpu.run(fo, 0.0, steps)
+    del cpu
+    gpu = gpu_stepper(case, "exact")
+    fg = torch.full((g.nz(), g.nr()), case.solver.T0, dtype=torch.float64, device="cuda").t()
+    te_g, _, res_g = gpu.run(fg, 0.0, steps, keep_results=True)
+    assert te_g == te_o
+    assert np.array_equal(_seq(res_g), _seq(res_o))
+    assert min(r.radial.iterations for r in res_o) >= 2  # nonlinear Picard work happened
+    m = g.mask()
+    got = to_host(fg)
+    assert np.array_equal(got[m], fo[m])
+    assert not np.array_equal(fo[m], make_field(g, case.solver.T0)[m])
+
+
 def test_fast_vs_exact_cfg3_full_size(cuda):
     """configs[3] at full size (8192 x 16384): fast vs exact (exact is bit-identical
     to the reference by the tests above), 3 steps, judged against the
