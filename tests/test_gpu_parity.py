@@ -706,6 +706,25 @@ def test_growth_controller_matches_oracle(cuda, name):
             assert _rel(to_host(fg), fo, g.mask()) <= ADAPTIVE_TOL
 
 
+@pytest.mark.parametrize("name,steps", [("cfg2", 8), ("cfg4", 4)])
+def test_growth_controller_full_size_exact(cuda, name, steps):
+    """configs[2] (1024 x 2048) and configs[4] (2048 x 4096 stepped cell) at their
+    full BASELINE sizes: the first steps of the growth controller, exact mode,
+    bit for bit against the C restatement (fields, dt, halvings, iterations,
+    last_delta)."""
+    case = configs.cfg2() if name == "cfg2" else configs.cfg4()
+    g = case.grid()
+    port = PortStepper(case)
+    fo = make_field(g, case.solver.T0)
+    t_o, _, res_o = port.run_growth(fo, 0.0, case.t_end, steps)
+    gpu = gpu_stepper(case, "exact")
+    fg = to_dev(make_field(g, case.solver.T0))
+    t_g, _, res_g = gpu.run_growth(fg, 0.0, case.t_end, steps, keep_results=True)
+    assert t_g == t_o and len(res_g) == steps
+    assert np.array_equal(_seq(res_g), _seq(res_o))
+    assert np.array_equal(to_host(fg)[g.mask()], fo[g.mask()])
+
+
 # ---- exact mode on the kernel variants the large configs select -------------
 def _cfg4s():
     return configs.scaled(configs.cfg4(), [44, 5, 13, 3], 128, 87)
