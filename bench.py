@@ -138,6 +138,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-supp", action="store_true",
+                    help="skip the supplementary configs[1] batched-Thomas measurement")
     ap.add_argument("--partitioned", action="store_true",
                     help="run the partitioned (multi-GPU) stepper even at world size 1 "
                          "(under torchrun: a 1-rank NCCL communicator; validation of that path)")
@@ -208,6 +210,7 @@ def main():
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     launches = stepper.launch_count() - launches0
+    kernels_desc = stepper.describe()
     kt = stepper.kernel_timing()
     stepper.enable_kernel_timing(False)
     ms_t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
@@ -302,6 +305,21 @@ def main():
                       "d2h_bytes_per_step": 8 * len(rcfg.probes),
                       "api": "runner.evolve (pcgpu_evolve: field resident, probes per step)"}
 
+    # Supplementary: configs[1], 131072 x 1024 batched Thomas solves in both
+    # layouts (tools/bench_tridiag.py: CUDA events, a sample checked bit for
+    # bit against the C restatement). A parity case, not the bench workload.
+    supp = None
+    if rank == 0 and world == 1 and not args.no_supp:
+        from tools.bench_tridiag import run as run_tridiag
+        del stepper
+        torch.cuda.empty_cache()
+        tri = run_tridiag()
+        supp = {"cfg1_tridiag": {"unit": "ms per batched solve (131072 x 1024)",
+                                 **{k: {kk: v[kk] for kk in ("ms", "GBps_algorithmic",
+                                                           "bitwise_vs_oracle_sample")}
+                                    for k, v in tri.items()}}}
+        stepper = None
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = run_reference_cpu(case, args.cpu_steps, 0, args.cpu_nz, os.cpu_count() or 1)
@@ -313,7 +331,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": dict(grid_desc, mode=args.mode, kernels=stepper.describe(),
+            "config": dict(grid_desc, mode=args.mode, kernels=kernels_desc,
                            parity="bit-identical to the reference" if args.mode == "exact"
                            else "reference rounding-noise floor",
                            parallelism=f"replicas x{world}",
@@ -334,7 +352,7 @@ def main():
                          "other_sweep_ms_per_launch": {k: v[0] / max(v[1], 1) for k, v in
                                                        sweeps.items()}},
             "cpu_baseline": cpu, "e2e": e2e, "e2e_runner": e2e_runner, "clocks": clk.summary(),
-            "gpu_launches": launches,
+            "gpu_launches": launches, "supplementary": supp,
         }
         print(json.dumps(line))
     if pg:

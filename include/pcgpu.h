@@ -392,7 +392,10 @@ int pcgpu_dist_timing(const pcgpu_dist* h, double* transpose_ms, int64_t* transp
  *   PCGPU_LAYOUT_STRIDED:    system s, row k at k*batch + s (interleaved / transposed)
  * lower[k=0] and upper[k=n-1] are ignored like the reference. x may alias rhs.
  * `exact` = 1: the reference's operation order, bit-identical per system;
- * 0: the fastest variant (may reorder arithmetic). Returns PCGPU_ERR_ZERO_PIVOT
+ * 0: the fastest variant (currently the same kernels). Contiguous layout only,
+ * for comparison: 2 = the legacy warp-tiled kernel, 3 = the transpose path
+ * (32x32 transposes around the strided kernel); otherwise the fused TMA kernel
+ * when n is even and the bands are 16-B aligned. Returns PCGPU_ERR_ZERO_PIVOT
  * (error_line = lowest failing system) on a zero pivot. */
 enum pcgpu_layout { PCGPU_LAYOUT_CONTIGUOUS = 0, PCGPU_LAYOUT_STRIDED = 1 };
 int pcgpu_tridiag_batch(const double* lower, const double* diag, const double* upper,
