@@ -373,6 +373,10 @@ int32_t pcgpu_dist_transport(const pcgpu_dist* h);
 #define PCGPU_DIST_IPC_BYTES 256
 int pcgpu_dist_ipc_export(pcgpu_dist* h, void* handles);
 int pcgpu_dist_ipc_import(pcgpu_dist* h, const void* all_handles);
+/* Close the imported peer mappings and return to the NCCL transport. The
+ * transport must be the same on every rank: when any rank's import failed,
+ * every rank calls this (the Python mirror agrees on it with an all-gather). */
+int pcgpu_dist_peer_off(pcgpu_dist* h);
 /* nsteps x step() with t += tau_used on the partitioned state. */
 int pcgpu_dist_run(pcgpu_dist* h, double t0, int32_t nsteps, pcgpu_step_result* results,
                    pcgpu_run_stats* stats);

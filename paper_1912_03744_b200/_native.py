@@ -91,7 +91,7 @@ EXPORTS = [
     "pcgpu_pipeline_stats",
     "pcgpu_dist_run", "pcgpu_dist_stream", "pcgpu_dist_enable_timing",
     "pcgpu_dist_timing", "pcgpu_dist_launch_count", "pcgpu_run_growth", "pcgpu_describe", "pcgpu_dist_transport",
-    "pcgpu_dist_ipc_export", "pcgpu_dist_ipc_import", "pcgpu_evolve", "pcgpu_detector_periods",
+    "pcgpu_dist_ipc_export", "pcgpu_dist_ipc_import", "pcgpu_dist_peer_off", "pcgpu_evolve", "pcgpu_detector_periods",
     "pcgpu_evolve_host",
     "pcgpu_writer_create", "pcgpu_writer_destroy", "pcgpu_writer_submit", "pcgpu_writer_flush",
     "pcgpu_writer_last_error",
@@ -174,6 +174,7 @@ def load():
         "pcgpu_dist_transport": (C.c_int32, [vp]),
         "pcgpu_dist_ipc_export": (C.c_int, [vp, vp]),
         "pcgpu_dist_ipc_import": (C.c_int, [vp, vp]),
+        "pcgpu_dist_peer_off": (C.c_int, [vp]),
         "pcgpu_dist_enable_timing": (C.c_int, [vp, C.c_int32]),
         "pcgpu_dist_timing": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                         C.POINTER(C.c_int64), C.POINTER(C.c_double),

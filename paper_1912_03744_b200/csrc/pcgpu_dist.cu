@@ -1029,7 +1029,13 @@ int pcgpu_dist_ipc_import(pcgpu_dist* h, const void* all_handles) {
         cudaIpcMemHandle_t m;
         std::memcpy(&m, in + (static_cast<size_t>(q) * 4 + k) * sizeof m, sizeof m);
         void* p = nullptr;
-        DCK(cudaIpcOpenMemHandle(&p, m, cudaIpcMemLazyEnablePeerAccess));
+        const cudaError_t ce = cudaIpcOpenMemHandle(&p, m, cudaIpcMemLazyEnablePeerAccess);
+        if (ce != cudaSuccess) {
+          (void)cudaGetLastError();
+          for (void* o : h->ipc_opened) cudaIpcCloseMemHandle(o);
+          h->ipc_opened.clear();
+          DCK(ce);
+        }
         h->ipc_opened.push_back(p);
         *dst[k] = static_cast<double*>(p);
       }
@@ -1040,6 +1046,17 @@ int pcgpu_dist_ipc_import(pcgpu_dist* h, const void* all_handles) {
     h->err = e.what;
     return e.code;
   }
+  return PCGPU_OK;
+}
+
+int pcgpu_dist_peer_off(pcgpu_dist* h) {
+  if (!h) return PCGPU_ERR_ARG;
+  if (h->local) return PCGPU_OK;  // emulated ranks: peer stores into local slabs
+  if (cudaSetDevice(h->d.device) != cudaSuccess) return PCGPU_ERR_CUDA;
+  cudaStreamSynchronize(h->stream);
+  for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
+  h->ipc_opened.clear();
+  h->peer = false;
   return PCGPU_OK;
 }
 

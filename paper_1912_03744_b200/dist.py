@@ -168,7 +168,16 @@ class PartitionedAdi:
         self._check(self._lib.pcgpu_dist_ipc_export(self._h, mine))
         blob = allgather_bytes(bytes(mine))
         allh = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
-        self._check(self._lib.pcgpu_dist_ipc_import(self._h, allh))
+        rc = self._lib.pcgpu_dist_ipc_import(self._h, allh)
+        # every rank must use the same transport: agree on the outcome
+        ok = allgather_bytes(bytes([1 if rc == N.OK else 0]))
+        if all(ok):
+            return True
+        self._check(self._lib.pcgpu_dist_peer_off(self._h))
+        import warnings
+        warnings.warn("pcgpu: CUDA IPC peer mapping failed on rank(s) "
+                      f"{[r for r, v in enumerate(ok) if not v]}; using the NCCL transport")
+        return False
 
     def stream(self) -> int:
         return int(self._lib.pcgpu_dist_stream(self._h) or 0)

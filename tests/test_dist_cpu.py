@@ -80,3 +80,64 @@ def test_gloo_world2_plan_and_unique_id():
         assert max(zc) - min(zc) <= 2 * g.nr()
         rc = [sum(g.col_extent(i) for i in range(a, b)) for a, b in zip(rb, rb[1:])]
         assert max(rc) - min(rc) <= 2 * g.nz()
+
+
+class _FakeLib:
+    """Stands in for libpcgpu's IPC entry points: rank `fail` cannot map its peers."""
+
+    def __init__(self, rank, fail):
+        self.rank, self.fail, self.calls = rank, fail, []
+
+    def pcgpu_dist_ipc_export(self, h, buf):
+        self.calls.append("export")
+        return 0
+
+    def pcgpu_dist_ipc_import(self, h, buf):
+        self.calls.append("import")
+        return 5 if self.rank == self.fail else 0
+
+    def pcgpu_dist_peer_off(self, h):
+        self.calls.append("peer_off")
+        return 0
+
+
+def _transport_worker(rank, world, port, fail, q):
+    import warnings
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1912_03744_b200.dist import PartitionedAdi
+        part = object.__new__(PartitionedAdi)
+        part._lib, part._h = _FakeLib(rank, fail), None
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            on = part.enable_peer_transport()
+        q.put((rank, (on, part._lib.calls)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail", [-1, 1])
+def test_gloo_world2_peer_transport_agreement(fail):
+    """The transport is agreed collectively: when one rank's CUDA IPC import
+    fails, every rank drops its peer mapping (pcgpu_dist_peer_off) and all of
+    them use the NCCL transport; otherwise all keep the peer transport."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_transport_worker, args=(r, world, port, fail, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        on, calls = res[r]
+        if fail < 0:
+            assert on is True and calls == ["export", "import"]
+        else:
+            assert on is False and calls == ["export", "import", "peer_off"]
