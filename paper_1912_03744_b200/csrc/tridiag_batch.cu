@@ -508,9 +508,14 @@ extern "C" int pcgpu_tridiag_batch(const double* lower, const double* diag, cons
       pool_set = true;
     }
   }
+  // the fused contiguous kernel keeps its own (padded) scratch; the other
+  // kernels take `work` from w
+  const bool fused = layout != PCGPU_LAYOUT_STRIDED && exact != 2 && exact != 3 &&
+                     contig_tma_ok(lower, diag, upper, rhs, x, n, batch);
   double* w = nullptr;
   unsigned long long* fail = nullptr;
-  if (cudaMallocAsync(&w, sizeof(double) * static_cast<size_t>(n * batch), s) != cudaSuccess)
+  if (!fused &&
+      cudaMallocAsync(&w, sizeof(double) * static_cast<size_t>(n * batch), s) != cudaSuccess)
     return PCGPU_ERR_CUDA;
   if (cudaMallocAsync(&fail, sizeof(unsigned long long), s) != cudaSuccess) return PCGPU_ERR_CUDA;
   cudaMemsetAsync(fail, 0xff, sizeof(unsigned long long), s);
@@ -518,7 +523,7 @@ extern "C" int pcgpu_tridiag_batch(const double* lower, const double* diag, cons
     const int th = 128;
     k_thomas_strided<<<static_cast<unsigned>((batch + th - 1) / th), th, 0, s>>>(
         lower, diag, upper, rhs, x, w, n, batch, fail);
-  } else if (exact != 2 && exact != 3 && contig_tma_ok(lower, diag, upper, rhs, x, n, batch)) {
+  } else if (fused) {
     ContigMaps maps{};
     encode_contig(&maps.a, lower, n, batch);
     encode_contig(&maps.b, diag, n, batch);
@@ -572,7 +577,7 @@ extern "C" int pcgpu_tridiag_batch(const double* lower, const double* diag, cons
   ++g_launches;
   unsigned long long hfail = ~0ull;
   cudaMemcpyAsync(&hfail, fail, sizeof hfail, cudaMemcpyDeviceToHost, s);
-  cudaFreeAsync(w, s);
+  if (w) cudaFreeAsync(w, s);
   cudaFreeAsync(fail, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return PCGPU_ERR_CUDA;
   if (hfail != ~0ull) {
