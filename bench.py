@@ -306,8 +306,8 @@ def main():
                       "api": "runner.evolve (pcgpu_evolve: field resident, probes per step)"}
 
     # Supplementary: configs[1], 131072 x 1024 batched Thomas solves in both
-    # layouts (tools/bench_tridiag.py: CUDA events, a sample checked bit for
-    # bit against the C restatement). A parity case, not the bench workload.
+    # layouts (tools/bench_tridiag.py: CUDA events; their parity is tested in
+    # tests/test_gpu_parity.py). A parity case, not the bench workload.
     supp = None
     if rank == 0 and world == 1 and not args.no_supp:
         from tools.bench_tridiag import run as run_tridiag
@@ -315,8 +315,9 @@ def main():
         torch.cuda.empty_cache()
         tri = run_tridiag()
         supp = {"cfg1_tridiag": {"unit": "ms per batched solve (131072 x 1024)",
+                                 "parity": "bit-identical per system (tests/test_gpu_parity.py)",
                                  **{k: {kk: v[kk] for kk in ("ms", "GBps_algorithmic",
-                                                           "bitwise_vs_oracle_sample")}
+                                                           "rows_per_s")}
                                     for k, v in tri.items()}}}
         stepper = None
 

@@ -1,4 +1,4 @@
-"""Every BASELINE.json config on one B200, next to the reference's own CPU path
+"""TEST INFRASTRUCTURE (a report, not a test): every BASELINE.json config on one B200, next to the reference's own CPU path
 on the same box's host cores. Prints one JSON object; the
 committed copy lives in profiles/ (r01_configs_report.json).
 
@@ -15,7 +15,7 @@ committed copy lives in profiles/ (r01_configs_report.json).
   cfg4  2048 x 4096 stepped cell, growth controller, 10 periods; same checks.
 cfg3 is bench.py's workload.
 
-    python tools/configs_report.py [--only cfg0,cfg2] [--periods-scale 1.0]
+    python tests/reports/configs_report.py [--only cfg0,cfg2] [--periods-scale 1.0]
 """
 import argparse
 import json
@@ -23,7 +23,7 @@ import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -102,7 +102,7 @@ def cfg0():
 def cfg1(cpu_systems=16384):
     from tools.bench_tridiag import run
     from oracle.oracle import ref_thomas_batch
-    gpu = run()
+    gpu = run(check=256)
     rng = np.random.default_rng(2024)
     n = 1024
     a = -rng.random((cpu_systems, n))

@@ -2,7 +2,9 @@
 diagonally dominant (sub/super ~ U[-1,0], diag = 2.05 + |sub| + |super|,
 rhs ~ U[-1,1]), in the line-contiguous and the strided layout. Times
 pcgpu_tridiag_batch (the reference's Thomas order, bit-identical per system)
-with CUDA events and checks a sample of systems against the C oracle.
+with CUDA events. The bit-for-bit check of a sample against the C restatement
+(`check` > 0) is for the test-side reports only (tests/reports/); bench.py runs
+it with check = 0 (the oracle is never imported there).
 
     python tools/bench_tridiag.py [--batch 131072] [--n 1024]
 Prints one JSON line.
@@ -19,7 +21,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 
-def run(batch=131072, n=1024, reps=5, seed=2024, check=256):
+def run(batch=131072, n=1024, reps=5, seed=2024, check=0):
     from paper_1912_03744_b200.tridiagonal import CONTIGUOUS, STRIDED, thomas_solve_batch
     g = torch.Generator(device="cuda").manual_seed(seed)
     shape = (batch, n)
@@ -48,13 +50,14 @@ def run(batch=131072, n=1024, reps=5, seed=2024, check=256):
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
         ms = float(np.median(times))
-        # check a sample against the C oracle (bitwise)
-        from oracle.oracle import port_thomas_batch
-        rows = slice(0, check)
-        sub = [t[rows].contiguous().view(-1).cpu().numpy() for t in (a, b, c, d)]
-        rc, xo, _ = port_thomas_batch(*sub, n, check, 0)
-        xg = (x.view(batch, n) if layout == CONTIGUOUS else x.view(n, batch).t())[rows]
-        bitwise = bool(np.array_equal(xg.contiguous().view(-1).cpu().numpy(), xo))
+        bitwise = None
+        if check > 0:  # test-side reports only: a sample against the C restatement
+            from oracle.oracle import port_thomas_batch
+            rows = slice(0, check)
+            sub = [t[rows].contiguous().view(-1).cpu().numpy() for t in (a, b, c, d)]
+            rc, xo, _ = port_thomas_batch(*sub, n, check, 0)
+            xg = (x.view(batch, n) if layout == CONTIGUOUS else x.view(n, batch).t())[rows]
+            bitwise = bool(np.array_equal(xg.contiguous().view(-1).cpu().numpy(), xo))
         out[name] = {"ms": ms, "GBps_algorithmic": bytes_per_solve / (ms / 1e3) / 1e9,
                      "rows_per_s": batch * n / (ms / 1e3), "bitwise_vs_oracle_sample": bitwise}
         del bands, x
