@@ -3,16 +3,20 @@
 HBM roofline (BASELINE.json metric) on configs[3] -- the large grid
 Nr=8192 x Nz=16384, fixed dt 1e-5 -- one JSON line on rank 0.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--mode exact|fast]
-
-The default mode is exact: bit-identical to the reference AdiStepper.
+  python bench.py [--gpus N] [--steps K] [--warmup W]
   python bench.py --impl reference   # the reference's own CPU AdiStepper
 
-A "step" is one accepted ADI time step (AdiStepper::step, solver.cpp:356-373)
-of the whole grid. Cell-updates count every half-step attempt's active cells x
-Picard iterations. Multi-GPU (torchrun): each rank advances its
-own replica of the grid (the z-slab partition is not wired into the bench
-yet), so the job is weak-scaled; time is the max over ranks.
+The kernels are bit-identical to the reference AdiStepper. A "step" is one
+accepted ADI time step (AdiStepper::step, solver.cpp:356-373) of the whole
+grid. Cell-updates count every half-step attempt's active cells x Picard
+iterations. Multi-GPU (torchrun, N > 1): the z-slab / r-slab
+partitioned stepper (run_partitioned) over the N GPUs -- total work fixed,
+strong scaling; time is the max over ranks.
+
+The CPU numbers (the reference arm and this arm's cpu_baseline) are the
+reference's own AdiStepper on the FULL configs[3] grid with bench.cpp:12-25
+semantics: one untimed warm-up step, then two timed step() calls on a
+LinePool of all host cores; plus a 1-worker row on a z-slice.
 """
 from __future__ import annotations
 
@@ -98,14 +102,14 @@ def cpu_sample_case(case, nz_sample: int):
                           name=case.name + f"-z{nz_sample}")
 
 
-def run_reference_cpu(case, steps: int, warmup: int, nz_sample: int, workers: int):
+def run_reference_cpu(case, steps: int, warmup: int, nz_sample, workers: int):
     """The reference's own AdiStepper (oracle/_ref, compiled from its sources)
     on a LinePool of `workers` threads: `warmup` untimed + `steps` timed step()
-    calls (bench.cpp:12-25 semantics) on a z-truncated sample."""
-    import numpy as np
+    calls (bench.cpp:12-25 semantics) on the full grid (nz_sample None) or a
+    z-truncated sample."""
     from oracle.oracle import RefStepper, ref_available, PortStepper
     from paper_1912_03744_b200.solver import make_field
-    sample = cpu_sample_case(case, nz_sample)
+    sample = case if nz_sample is None else cpu_sample_case(case, nz_sample)
     g = sample.grid()
     if ref_available():
         stepper, kind = RefStepper(sample, workers=workers), "reference"
@@ -118,11 +122,24 @@ def run_reference_cpu(case, steps: int, warmup: int, nz_sample: int, workers: in
     t0 = time.perf_counter()
     t_end, stats, _ = stepper.run(f, t, steps)
     dt = time.perf_counter() - t0
+    what = (f"the full {g.nr()}x{g.nz()} {case.name} grid" if nz_sample is None else
+            f"{g.nr()}x{g.nz()} z-slice of {case.name} (same radial lines, materials, tau)")
     return {"value": stats["cell_updates"] / dt, "unit": "cell-updates/s", "cores": workers,
             "kind": kind, "seconds": dt,
-            "sample": f"{g.nr()}x{g.nz()} z-slice of {case.name} (same radial lines, materials, "
-                      f"tau), {warmup} warm-up + {steps} timed step() calls, "
-                      f"{stats['cell_updates']:.3e} cell-updates"}
+            "sample": f"{what}, {warmup} warm-up + {steps} timed step() calls "
+                      f"(bench.cpp:12-25), {stats['cell_updates']:.3e} cell-updates"}
+
+
+def cpu_rows(case, nz_sample=None):
+    """The CPU baseline of both arms: all host cores on the full grid, and a
+    1-worker row on a 1024-row z-slice (bounded run time). nz_sample: a
+    z-slice instead of the full grid (the CPU test suite's quick check)."""
+    full = run_reference_cpu(case, 2, 1, nz_sample, os.cpu_count() or 1)
+    one = run_reference_cpu(case, 1, 0, min(1024, nz_sample or 1024), 1)
+    keys = ("value", "unit", "cores", "kind", "sample")
+    out = {k: full[k] for k in keys}
+    out["one_worker"] = {k: one[k] for k in keys}
+    return out
 
 
 def main():
@@ -131,12 +148,10 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default=os.environ.get("PCGPU_BENCH_MODE", "exact"),
-                    choices=["exact", "fast"])
     ap.add_argument("--config", default="cfg3")
-    ap.add_argument("--cpu-nz", type=int, default=512, help="z-slice of the CPU sample")
-    ap.add_argument("--cpu-steps", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-nz", type=int, default=None,
+                    help="CPU legs on a z-slice of this many rows (tests); default the full grid")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-supp", action="store_true",
                     help="skip the supplementary configs[1] batched-Thomas measurement")
@@ -156,14 +171,15 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        workers = os.cpu_count() or 1
-        r = run_reference_cpu(case, max(1, args.steps // 10 or 1), min(args.warmup, 1),
-                              args.cpu_nz, workers)
+        r = cpu_rows(case, args.cpu_nz)
         line = {"impl": "reference", "metric": metric, "value": r["value"],
-                "unit": "cell-updates/s", "n_gpus": args.gpus, "steps": args.steps,
-                "warmup": args.warmup, "higher_is_better": True, "dtype": "f64",
-                "data": "synthetic", "config": dict(grid_desc, parallelism="cpu LinePool"),
-                "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "unit": "cell-updates/s", "n_gpus": args.gpus, "steps": 2,
+                "warmup": 1, "higher_is_better": True, "dtype": "f64",
+                "data": "synthetic",
+                "config": dict(grid_desc, parallelism=f"cpu LinePool x{r['cores']}",
+                               note="bench.cpp semantics: 1 untimed warm-up + 2 timed steps "
+                                    "of the full grid, whatever --steps/--warmup say"),
+                "cpu_baseline": r,
                 "e2e": {"value": r["value"], "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
@@ -186,7 +202,7 @@ def main():
         run_partitioned(args, case, rank, world, local, pg, grid_desc, metric)
         pg.destroy_process_group()
         return
-    stepper = gpu_stepper_for(case, args.mode, local)
+    stepper = gpu_stepper_for(case, local)
     field = torch.full((nz, nr), case.solver.T0, dtype=torch.float64, device=f"cuda:{local}").t()
     t = 0.0
     # warm-up steps (untimed)
@@ -233,7 +249,7 @@ def main():
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            tr = json.load(f).get(f"{args.config}:{args.mode}:{dom}")
+            tr = json.load(f).get(f"{args.config}:exact:{dom}")
         if tr:
             traffic = tr["dram_bytes_per_launch"] / 1e9
             traffic_src = tr.get("source")
@@ -323,8 +339,9 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = run_reference_cpu(case, args.cpu_steps, 0, args.cpu_nz, os.cpu_count() or 1)
-        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        del stepper, field
+        torch.cuda.empty_cache()
+        cpu = cpu_rows(case, args.cpu_nz)
 
     if rank == 0:
         line = {
@@ -332,9 +349,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": dict(grid_desc, mode=args.mode, kernels=kernels_desc,
-                           parity="bit-identical to the reference" if args.mode == "exact"
-                           else "reference rounding-noise floor",
+            "config": dict(grid_desc, kernels=kernels_desc,
+                           parity="bit-identical to the reference",
                            parallelism=f"replicas x{world}",
                            l2="inputs > L2 (1 GiB FP64 fields)",
                            picard={"radial_iters": stats["radial_iterations"],
@@ -347,7 +363,7 @@ def main():
                          # (80 B per cell: the exact Thomas working set)
                          "traffic_frac": (traffic / (dom_ms / max(dom_n, 1) / 1e3) / peak
                                           if traffic and dom_n else None),
-                         "kernel": f"{dom} Picard iteration ({args.mode})",
+                         "kernel": f"{dom} Picard iteration",
                          "bytes_per_launch": per_launch_bytes, "launches": dom_n,
                          "ms_per_launch": dom_ms / max(dom_n, 1), "peak_kind": peak_kind,
                          "other_sweep_ms_per_launch": {k: v[0] / max(v[1], 1) for k, v in
@@ -371,8 +387,8 @@ def run_partitioned(args, case, rank, world, local, pg, grid_desc, metric):
     dev = torch.device(f"cuda:{local}")
     uid = share_unique_id(rank, dev)
     part = PartitionedAdi(g, case.materials, make_source(case, g), case.timing, case.solver,
-                          device=local, rank=rank, world=world, unique_id=uid, mode=args.mode)
-    if args.mode == "exact" and os.environ.get("PCGPU_DIST_TRANSPORT", "peer") != "nccl":
+                          device=local, rank=rank, world=world, unique_id=uid)
+    if os.environ.get("PCGPU_DIST_TRANSPORT", "peer") != "nccl":
         part.enable_peer_transport()  # fused K3/K4 + peer stores over NVLink
     field = torch.full((g.nz(), g.nr()), case.solver.T0, dtype=torch.float64, device=dev).t()
     part.set_field(field)
@@ -416,7 +432,7 @@ def run_partitioned(args, case, rank, world, local, pg, grid_desc, metric):
     # step each rank copies its state lines (1/world of the field) in from
     # pinned host memory and back out, over its own PCIe link
     e2e = None
-    if not args.no_e2e and args.mode == "exact":
+    if not args.no_e2e:
         part.enable_timing(False)
         host_t = torch.full((g.nz(), g.nr()), case.solver.T0, dtype=torch.float64).pin_memory()
         hp = host_t.numpy().T  # (nr, nz) Fortran view of pinned memory
@@ -453,14 +469,14 @@ def run_partitioned(args, case, rank, world, local, pg, grid_desc, metric):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": dict(grid_desc, mode=args.mode, parallelism=f"z-slab/r-slab x{world}",
+            "config": dict(grid_desc, parallelism=f"z-slab/r-slab x{world}",
                            transport=part.transport(),
                            l2="inputs > L2", rank0_slabs={"z": [z0, z1], "r": [r0, r1]},
                            picard={"radial_iters": stats["radial_iterations"],
                                    "axial_iters": stats["axial_iterations"],
                                    "halvings": stats["halvings"]}),
             "transpose": {"ms_per_transpose_max_rank": float(tr.item()),
-                          "transposes_per_step": 3 if args.mode == "exact" else 2,
+                          "transposes_per_step": 3,
                           "fields_per_step": 4,
                           "bytes_per_rank_per_step":
                               4 * 8 * g.nr() * g.nz() // world * (world - 1) // world},
@@ -469,12 +485,12 @@ def run_partitioned(args, case, rank, world, local, pg, grid_desc, metric):
         print(json.dumps(line))
 
 
-def gpu_stepper_for(case, mode, device):
+def gpu_stepper_for(case, device):
     from paper_1912_03744_b200.configs import make_source
     from paper_1912_03744_b200.solver import AdiStepper, DevicePlan
     g = case.grid()
     return AdiStepper(g, case.materials, make_source(case, g), case.timing, case.solver,
-                      DevicePlan(device=device, mode=mode))
+                      DevicePlan(device=device))
 
 
 if __name__ == "__main__":

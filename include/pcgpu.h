@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define PCGPU_ABI_VERSION 2
+#define PCGPU_ABI_VERSION 3
 
 /* Status codes. Reference equivalents in brackets. */
 enum pcgpu_status {
@@ -55,11 +55,11 @@ enum pcgpu_source_kind {
 };
 enum pcgpu_mode {
   /* Bit-identical to the reference CPU path: the reference's operation order
-   * (SURVEY Appendix A), no FMA contraction, sequential Thomas per line. */
-  PCGPU_MODE_EXACT = 0,
-  /* Throughput mode: partitioned (chunked) line solves, FMA allowed. Agrees with
-   * the reference to roundoff (north-star tolerance 1e-9 fixed-dt / 1e-6 adaptive). */
-  PCGPU_MODE_FAST = 1
+   * (SURVEY Appendix A), no FMA contraction, sequential Thomas per line. The
+   * only mode (the round-1 partitioned "fast" line solver is retired: off the
+   * bit-exact path it cannot meet the 1e-9 fixed-dt bar on the stiff grids,
+   * DESIGN.md section 4.2). */
+  PCGPU_MODE_EXACT = 0
 };
 
 /* Piecewise-linear property table: n strictly increasing knots t[] and values v[]
@@ -185,6 +185,28 @@ double pcgpu_pulse_value(const pcgpu_stepper* h, double t);
 /* Active cells of the grid (Grid::active_cells, geometry.cpp:95). */
 int64_t pcgpu_active_cells(const pcgpu_stepper* h);
 
+/* The host functions behind the time stepping: pulse_value(t, spec)
+ * (source.cpp:42-45) and initial_tau(t, timing, cfg) (solver.cpp:44-51). By
+ * default the library uses its own restatements; a caller holding the
+ * reference objects (the C++ drop-in) passes the reference's functions here so
+ * that the stepper runs on exactly the reference's host arithmetic. Either
+ * pointer may be NULL (keep the default). */
+typedef double (*pcgpu_clock_fn)(void* user, double t);
+int pcgpu_set_host_clock(pcgpu_stepper* h, pcgpu_clock_fn pulse_value, pcgpu_clock_fn initial_tau,
+                         void* user);
+/* After PCGPU_ERR_TAU_FLOOR: TauFloorError's tau(), floor() and time()
+ * (errors.hpp, solver.cpp:371). */
+int pcgpu_last_tau_floor(const pcgpu_stepper* h, double* tau, double* floor, double* t);
+
+/* Resident stepper (whole steps -- tau controller, Picard loops with their
+ * device max-norm tests, accept-or-halve -- in one cooperative launch per
+ * batch of steps; used by pcgpu_step / pcgpu_run / pcgpu_run_growth /
+ * pcgpu_evolve on grids of at most one 32-line block per SM and sweep;
+ * $PCGPU_RESIDENT=0 disables it): grid size (0 = not used), batches launched,
+ * steps they accepted, steps redone host-driven (> 8 halvings in one step). */
+int pcgpu_resident_stats(const pcgpu_stepper* h, int32_t* grid, int64_t* batches, int64_t* steps,
+                         int64_t* host_steps);
+
 /* Per-cell power for PCGPU_SOURCE_FIELD: device pointer, nr x nz column-major,
  * read by the next half-step (the SourceModel::power(i, j, ...) values for the
  * half-step's bind_time). */
@@ -272,6 +294,15 @@ typedef struct pcgpu_runner_cfg {
   int32_t detector_min_periods;
   double detector_tolerance;
   int32_t source_on; /* SourceSpec::I0 > 0: regime detection engages with >= 1 probe */
+  /* The regime detector: NULL = the library's restatement of
+   * PhaseResampler / RegimeDetector (runner.cpp:35-95); otherwise the
+   * caller's (the C++ drop-in passes the reference's own RegimeDetector),
+   * called with seed = 1 once at t = 0 (RegimeDetector::seed), then with
+   * seed = 0 after every accepted step (RegimeDetector::update), returning
+   * nonzero when the periodic criterion fires. pcgpu_detector_periods then
+   * reports nothing (the caller's detector holds the periods). */
+  int32_t (*detect)(void* user, int32_t seed, double t, double v);
+  void* detect_user;
 } pcgpu_runner_cfg;
 
 typedef enum { PCGPU_STOP_REACHED_TIME = 0, PCGPU_STOP_PERIODIC = 1, PCGPU_STOP_TAU_FLOOR = 2 } pcgpu_stop;
@@ -331,8 +362,8 @@ const char* pcgpu_writer_last_error(const pcgpu_writer* w);
 /* ---- Partitioned stepper: one node of B200s ------------------
  * z-slabs (radial lines j) for the radial sweep, r-slabs (axial lines i) for
  * the axial sweep, all-to-all transposes between them, allreduce(max) of the
- * Picard norm every iteration. Exact mode (bit-identical to the single-GPU
- * exact stepper) or fast mode (bit-identical to a single-GPU fast run). With nccl_id == NULL the library emulates
+ * Picard norm every iteration, bit-identical to the single-GPU stepper. With
+ * nccl_id == NULL the library emulates
  * `nranks` ranks in this process on desc->device (test/validation mode);
  * otherwise this process is rank `rank` of an NCCL communicator created from
  * the 128-byte id produced by pcgpu_nccl_unique_id on one rank and shared by
@@ -351,8 +382,8 @@ int pcgpu_dist_plan(const pcgpu_desc* desc, int32_t nranks, int32_t* zb, int32_t
 int pcgpu_dist_slabs(const pcgpu_dist* h, int32_t* z0, int32_t* z1, int32_t* r0, int32_t* r1);
 /* Every rank passes the full initial field (device, nr x nz column-major). */
 int pcgpu_dist_set_field(pcgpu_dist* h, const double* field_dev);
-/* Writes this process's lines into the full-size device field: the r-slab
- * columns (axial lines) in exact mode, the z-slab rows in fast mode. */
+/* Writes this process's lines -- the r-slab columns (axial lines) -- into the
+ * full-size device field. */
 int pcgpu_dist_get_field(pcgpu_dist* h, double* field_dev);
 /* Exact mode, host fields (nr x nz column-major, ideally pinned): copy only
  * this process's state lines -- the r-slab columns (axial lines) -- in from /

@@ -9,6 +9,8 @@
 // the reference borrows them; their data are marshalled once into a
 // pcgpu_desc. Device-native sources: NullSource and JouleSource (recognised by
 // dynamic_cast, source.hpp:57-83); anything else is rejected with ConfigError.
+// The time stepping runs on the reference's own host functions (pulse_value,
+// initial_tau), registered with pcgpu_set_host_clock.
 //
 // Usage inside the reference tree:
 //   #include "pulsecell_gpu/adi_stepper.hpp"
@@ -32,8 +34,7 @@ namespace pulsecell {
 namespace gpu {
 
 struct DeviceOptions {
-  int device = 0;
-  bool exact = true;  // bit-identical to the CPU AdiStepper; false = throughput mode
+  int device = 0;  // CUDA device ordinal (the kernels are bit-identical to the CPU AdiStepper)
 };
 
 class AdiStepper {
@@ -108,10 +109,13 @@ class AdiStepper {
     d.all_neumann = cfg_.all_neumann ? 1 : 0;
     d.T0 = cfg_.T0;
     d.t_ceiling = cfg_.t_ceiling;
-    d.mode = opt.exact ? PCGPU_MODE_EXACT : PCGPU_MODE_FAST;
+    d.mode = PCGPU_MODE_EXACT;
     d.device = opt.device;
     const int rc = pcgpu_create(&d, &h_);
     if (rc != PCGPU_OK) raise(rc, pcgpu_last_error(nullptr));
+    // the reference's own host functions drive the time stepping:
+    // pulse_value (source.cpp:42-45) and initial_tau (solver.cpp:44-51)
+    pcgpu_set_host_clock(h_, &AdiStepper::pulse_cb, &AdiStepper::tau_cb, this);
   }
   ~AdiStepper() { pcgpu_destroy(h_); }
   AdiStepper(const AdiStepper&) = delete;
@@ -142,6 +146,13 @@ class AdiStepper {
   pcgpu_stepper* handle() { return h_; }
 
  private:
+  static double pulse_cb(void* u, double t) {
+    return pulse_value(t, static_cast<const AdiStepper*>(u)->timing_);
+  }
+  static double tau_cb(void* u, double t) {
+    const AdiStepper* s = static_cast<const AdiStepper*>(u);
+    return initial_tau(t, s->timing_, s->cfg_);
+  }
   static pcgpu_table table(const PropertyTable& t) {
     return pcgpu_table{static_cast<int32_t>(t.size()), t.empty() ? nullptr : t.knots().data(),
                        t.empty() ? nullptr : t.values().data()};
@@ -157,7 +168,11 @@ class AdiStepper {
     const std::string m = msg ? msg : "";
     switch (rc) {
       case PCGPU_ERR_CONFIG: throw ConfigError(m);
-      case PCGPU_ERR_TAU_FLOOR: throw TauFloorError(0, 0, 0);
+      case PCGPU_ERR_TAU_FLOOR: {  // TauFloorError(tau, floor, t) as solver.cpp:371 throws it
+        double tau = 0, floor = 0, t = 0;
+        if (h_) pcgpu_last_tau_floor(h_, &tau, &floor, &t);
+        throw TauFloorError(tau, floor, t);
+      }
       case PCGPU_ERR_TABLE_RANGE:
         throw LineError(h_ ? pcgpu_error_line(h_) : -1, "TableRangeError: " + m);
       case PCGPU_ERR_ZERO_PIVOT:
@@ -183,7 +198,8 @@ class AdiStepper {
 /// pulsecell::evolve (runner.cpp:97-190) for the GPU stepper, with the same
 /// arguments and EvolutionResult: the field stays on the device for the whole
 /// run (pcgpu_evolve_host); only probe values cross each step and snapshots
-/// when they occur. The probe cells are the reference's own probe_cell.
+/// when they occur. The probe cells are the reference's own probe_cell, and
+/// the regime detection is the reference's own RegimeDetector.
 inline EvolutionResult evolve(AdiStepper& stepper, const SourceSpec& timing, Array2 initial,
                               Real t_end, const RunnerConfig& cfg) {
   cfg.validate();
@@ -207,6 +223,17 @@ inline EvolutionResult evolve(AdiStepper& stepper, const SourceSpec& timing, Arr
   c.detector_min_periods = cfg.detector.min_periods;
   c.detector_tolerance = cfg.detector.tolerance;
   c.source_on = timing.I0 > 0;
+  // the reference's own RegimeDetector (runner.cpp:35-95) over probe 0
+  RegimeDetector detector(timing.t_per, cfg.detector);
+  c.detect = [](void* u, int32_t seed, double t, double v) -> int32_t {
+    RegimeDetector* d = static_cast<RegimeDetector*>(u);
+    if (seed) {
+      d->seed(t, v);
+      return 0;
+    }
+    return d->update(t, v) ? 1 : 0;
+  };
+  c.detect_user = &detector;
   EvolutionResult res;
   res.field = std::move(initial);
   struct Sink {
@@ -240,16 +267,7 @@ inline EvolutionResult evolve(AdiStepper& stepper, const SourceSpec& timing, Arr
   res.reason = static_cast<StopReason>(out.reason);
   res.fire_t = out.fire_t;
   if (res.reason == StopReason::TauFloor) res.error = pcgpu_last_error(stepper.handle());
-  if (out.detector_periods > 0) {
-    const int s = cfg.detector.samples_per_period;
-    std::vector<double> rows(static_cast<size_t>(out.detector_periods) * s);
-    pcgpu_detector_periods(stepper.handle(), rows.data(), out.detector_periods);
-    for (int k = 0; k < out.detector_periods; ++k) {
-      Vector v(s);
-      for (int q = 0; q < s; ++q) v[q] = rows[static_cast<size_t>(k) * s + q];
-      res.detector_periods.push_back(std::move(v));
-    }
-  }
+  if (c.source_on && !pi.empty()) res.detector_periods = detector.resampler().periods();
   return res;
 }
 

@@ -13,13 +13,13 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libpcgpu.so")
 
-PCGPU_ABI_VERSION = 2
+PCGPU_ABI_VERSION = 3
 DIST_IPC_BYTES = 256
 
 # pcgpu_status
 OK, ERR_CONFIG, ERR_TAU_FLOOR, ERR_TABLE_RANGE, ERR_ZERO_PIVOT, ERR_CUDA, ERR_ARG = range(7)
 # enums
-MODE_EXACT, MODE_FAST = 0, 1
+MODE_EXACT = 0
 SOURCE_NULL, SOURCE_JOULE, SOURCE_FIELD = 0, 1, 2
 LAYOUT_CONTIGUOUS, LAYOUT_STRIDED = 0, 1
 STOP_REACHED_TIME, STOP_PERIODIC, STOP_TAU_FLOOR = 0, 1, 2
@@ -81,7 +81,8 @@ class RunStats(C.Structure):
 EXPORTS = [
     "pcgpu_abi_version", "pcgpu_device_count", "pcgpu_create", "pcgpu_destroy",
     "pcgpu_last_error", "pcgpu_error_line", "pcgpu_initial_tau", "pcgpu_pulse_value",
-    "pcgpu_active_cells", "pcgpu_bind_power_field", "pcgpu_radial_half_step",
+    "pcgpu_active_cells", "pcgpu_set_host_clock", "pcgpu_last_tau_floor",
+    "pcgpu_resident_stats", "pcgpu_bind_power_field", "pcgpu_radial_half_step",
     "pcgpu_axial_half_step", "pcgpu_step", "pcgpu_step_host", "pcgpu_radial_half_step_host",
     "pcgpu_axial_half_step_host", "pcgpu_run", "pcgpu_clamp_events", "pcgpu_stream",
     "pcgpu_kernel_timing", "pcgpu_enable_kernel_timing", "pcgpu_launch_count",
@@ -96,6 +97,8 @@ EXPORTS = [
     "pcgpu_writer_create", "pcgpu_writer_destroy", "pcgpu_writer_submit", "pcgpu_writer_flush",
     "pcgpu_writer_last_error",
 ]
+
+CLOCK_FN = C.CFUNCTYPE(C.c_double, C.c_void_p, C.c_double)
 
 _lib = None
 
@@ -121,6 +124,11 @@ def load():
         "pcgpu_initial_tau": (C.c_double, [vp, C.c_double]),
         "pcgpu_pulse_value": (C.c_double, [vp, C.c_double]),
         "pcgpu_active_cells": (C.c_int64, [vp]),
+        "pcgpu_set_host_clock": (C.c_int, [vp, CLOCK_FN, CLOCK_FN, vp]),
+        "pcgpu_last_tau_floor": (C.c_int, [vp, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                           C.POINTER(C.c_double)]),
+        "pcgpu_resident_stats": (C.c_int, [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int64),
+                                           C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
         "pcgpu_bind_power_field": (C.c_int, [vp, vp]),
         "pcgpu_radial_half_step": (C.c_int, [vp, vp, C.c_double, C.c_double, vp,
                                              C.POINTER(Outcome)]),

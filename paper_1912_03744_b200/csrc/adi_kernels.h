@@ -89,35 +89,83 @@ void launch_rhs_zslab_scatter(const DevProblem& P, double pulse, int j0, int nj,
 void launch_transpose_N2T(const DevProblem& P, const double* srcN, double* dstT, cudaStream_t s);
 void launch_transpose_T2N(const DevProblem& P, const double* srcT, double* dstN, cudaStream_t s);
 
-// ---- fast mode (adi_fast.cu): partitioned line solves on contiguous lines ----
-bool fast_supported(const DevProblem& P);
-// K3: explN = Lambda_z[field] and TcN = field (from the T-layout field).
-void launch_explicit_axial_fast(const DevProblem& P, const double* fieldT, double* explN,
-                                double* TcN, DevStatus* st, cudaStream_t s);
-// K1: radial Picard iteration on N-layout lines.
-void launch_radial_fast(const DevProblem& P, int it, double eps, double half_k, double pulse,
-                        const double* TsN, const double* TcN, const double* explN,
-                        const double* powN, double* outN, DevStatus* st, cudaStream_t s);
-// K4: explT = Lambda_r[half] + X(half) and halfT = half (from the N-layout half field).
-void launch_axial_rhs_fast(const DevProblem& P, double pulse, const double* halfN,
-                           const double* powN, double* explT, double* halfT, DevStatus* st,
-                           cudaStream_t s);
-// K2: axial Picard iteration on T-layout lines (K-bar recomputed from the anchor).
-void launch_axial_fast(const DevProblem& P, int it, double eps, double half_k, const double* TsT,
-                       const double* ThT, const double* explT, double* outT, DevStatus* st,
-                       cudaStream_t s);
+// ---- resident stepper: a batch of whole steps in one cooperative launch ----
+// The tau controller, the Picard loops and their max-norm convergence tests,
+// the accept-or-halve decision and the field-buffer rotation all run on the
+// device; phases (K3, Picard iterations, K4) are separated by grid-wide
+// barriers. The host supplies a schedule -- per step t, the first attempt's
+// tau and pulse_value(t + tau_h / 2) for h = 0..kResHalv halvings, computed
+// by the host functions the reference uses -- that assumes no halvings; a
+// batch therefore ends after the first step that halved (its successors'
+// times change) and the host resumes from the device state.
+constexpr int kResHalv = 8;     // halvings with a precomputed pulse per step
+constexpr int kResProbes = 16;  // probe values gathered per step (evolve)
+constexpr int kResThreads = 384;
+struct ResSched {
+  double tau0;
+  double pulse[kResHalv + 1];
+};
+struct ResLog {
+  pcgpu_step_result r;
+  double updates;  // active cells x Picard iterations over every attempt
+  double probes[kResProbes];
+};
+enum ResStop { kResRan = 0, kResHalved = 1, kResError = 2, kResFloor = 3, kResNeedHost = 4 };
+struct ResCtl {
+  int steps;  // accepted steps of the batch
+  int stop;   // ResStop
+  int state;  // index of the field buffer after the last accepted step
+  int pad;
+  unsigned long long err;  // kResError: the line error word (line << 3 | code)
+  double tau;              // kResFloor: the attempt's tau below the floor
+  double updates;          // kResError / kResFloor / kResNeedHost: the failed step's work
+  unsigned long long clamp_save[kMaxLayers];
+  // phase profile (lead thread, %globaltimer ns; ResArgs::profile): time and
+  // count per phase -- 0 status reset, 1 K3, 2 radial iteration, 3 K4,
+  // 4 axial iteration, 5 step epilogue
+  unsigned long long prof_ns[8], prof_n[8];
+};
+struct ResArgs {
+  double* X[3];  // N-layout field rotation: X[state] is the field
+  double *TcT, *ExplT, *HalfT;  // radial anchor / explicit term / iterate (T); K4 -> HalfN, ExplN
+  double* kbarN;                // nullptr: K-bar computed in the axial sweep
+  double *W, *Xs;               // Thomas scratch
+  DevStatus* st2;               // [2] status, alternating per half-step
+  const ResSched* sched;
+  ResLog* log;
+  ResCtl* ctl;
+  const int* probe_off;  // [n_probes] N-layout offsets
+  int n_probes;
+  int nsteps, state0;
+  int max_iter, max_halv;  // max_halv <= kResHalv (lower: tests of the host redo)
+  int profile;             // record ResCtl::prof_*
+  int short_r, short_a;    // the sweep's lines fit the shared-memory (w, x) variant
+  double eps, tau_floor, active;
+};
+// Whether the resident stepper applies (exact-x / exact-lean lookups, no FIELD
+// source, <= kResProbes probes) and its grid size (0: not co-resident).
+int resident_grid(const DevProblem& P);
+void launch_resident(const DevProblem& P, const ResArgs& A, int grid, cudaStream_t s);
 
-// ---- partitioned (multi-GPU) slabs, fast mode (adi_fast.cu) ----
-void launch_radial_fast_slab(const DevProblem& P, int it, double eps, double half_k, double pulse,
-                             int j0, int nj, const double* TsN, const double* TcN,
-                             const double* explN, double* outN, DevStatus* st, cudaStream_t s);
-void launch_axial_fast_slab(const DevProblem& P, int it, double eps, double half_k, int i0,
-                            int ni, const double* TsT, const double* ThT, const double* explT,
-                            double* outT, DevStatus* st, cudaStream_t s);
-void launch_rhs_zslab(const DevProblem& P, double pulse, int j0, int nj, const double* hN,
-                      double* eN, DevStatus* st, cudaStream_t s);
-void launch_expl_rslab(const DevProblem& P, int i0, int ni, const double* fT, double* eT,
-                       DevStatus* st, cudaStream_t s);
+// Selects `dev` for the scope of an entry point and restores the caller's
+// current device afterwards (the library never leaves the current device
+// changed; every entry point works on its stepper's own device).
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true, changed = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) {
+      ok = cudaSetDevice(dev) == cudaSuccess;
+      changed = ok && prev >= 0;
+    }
+  }
+  ~DeviceGuard() {
+    if (changed) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
 
 // Kernel launch counter (for the bench's gpu_launches claim).
 extern unsigned long long g_launches;

@@ -15,8 +15,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/pcgpu.h"
@@ -126,9 +128,7 @@ std::string validate(const pcgpu_desc* d) {
   } else if (d->source_kind != PCGPU_SOURCE_NULL && d->source_kind != PCGPU_SOURCE_FIELD) {
     return "source: unknown kind";
   }
-  if (d->mode != PCGPU_MODE_EXACT && d->mode != PCGPU_MODE_FAST) return "pcgpu: unknown mode";
-  if (d->mode == PCGPU_MODE_FAST && (d->nr > 16384 || d->nz > 16384))
-    return "pcgpu: fast mode supports lines of up to 16384 cells";
+  if (d->mode != PCGPU_MODE_EXACT) return "pcgpu: unknown mode (only exact mode exists)";
   return "";
 }
 
@@ -220,8 +220,38 @@ struct pcgpu_stepper {
   double* pipe_spare = nullptr;       // third rotating radial iterate (T)
   const double* pipe_host = nullptr;  // set by pcgpu_step_host for its first attempt
   int64_t pipe_steps = 0, pipe_fallbacks = 0;
+  // resident stepper (whole steps in one cooperative launch per batch):
+  // grid size (0: not applicable), device control block, schedule and log
+  static constexpr int kResBatch = 1024;
+  int res_grid = 0;
+  ResCtl* res_ctl = nullptr;       // device
+  ResCtl* res_ctl_host = nullptr;  // pinned
+  ResSched* res_sched = nullptr;   // device [kResBatch]
+  ResSched* res_sched_host = nullptr;
+  ResLog* res_log = nullptr;       // device [kResBatch]
+  ResLog* res_log_host = nullptr;
+  DevStatus* res_st2 = nullptr;    // device [2]
+  int* res_probe_off = nullptr;    // device [kResProbes]
+  int64_t res_batches = 0, res_steps = 0, res_host_steps = 0;
+  // $PCGPU_RES_PROF=1: per-phase device time of the resident batches,
+  // printed to stderr when the stepper is destroyed
+  bool res_profile = std::getenv("PCGPU_RES_PROF") != nullptr;
+  double res_prof_ns[8] = {}, res_prof_n[8] = {};
+  // the host functions behind the schedule (the reference's own through
+  // pcgpu_set_host_clock, else the restatements below)
+  pcgpu_clock_fn pulse_fn = nullptr, tau_fn = nullptr;
+  void* clock_user = nullptr;
 
   ~pcgpu_stepper() {
+    if (res_profile && res_batches) {
+      static const char* names[6] = {"start", "K3", "radial_it", "K4", "axial_it", "epilogue"};
+      std::fprintf(stderr, "pcgpu resident profile (%lld batches, %lld steps):",
+                   static_cast<long long>(res_batches), static_cast<long long>(res_steps));
+      for (int q = 0; q < 6; ++q)
+        std::fprintf(stderr, " %s %.2f us x %.0f;", names[q],
+                     res_prof_n[q] ? res_prof_ns[q] / res_prof_n[q] / 1e3 : 0.0, res_prof_n[q]);
+      std::fprintf(stderr, "\n");
+    }
     delete runner;
     if (stream) cudaStreamSynchronize(stream);
     if (copy_stream) {
@@ -238,6 +268,9 @@ struct pcgpu_stepper {
     for (auto& e : chunk_done)
       if (e) cudaEventDestroy(e);
     if (st_pipe_host) cudaFreeHost(st_pipe_host);
+    if (res_ctl_host) cudaFreeHost(res_ctl_host);
+    if (res_sched_host) cudaFreeHost(res_sched_host);
+    if (res_log_host) cudaFreeHost(res_log_host);
     for (auto& e : ev_pool) cudaEventDestroy(e);
     for (void* p : dev_allocs) cudaFree(p);
     if (st_host) cudaFreeHost(st_host);
@@ -294,7 +327,12 @@ struct pcgpu_stepper {
 
   double pulse_for(double t, double tau) const {
     // SourceModel::bind_time(t + tau/2) (solver.cpp:238, :337)
-    return d.source_kind == PCGPU_SOURCE_JOULE ? host_pulse_value(d, t + 0.5 * tau) : 0.0;
+    if (d.source_kind != PCGPU_SOURCE_JOULE) return 0.0;
+    const double tb = t + 0.5 * tau;
+    return pulse_fn ? pulse_fn(clock_user, tb) : host_pulse_value(d, tb);
+  }
+  double initial_tau(double t) const {  // solver.cpp:44-51
+    return tau_fn ? tau_fn(clock_user, t) : host_initial_tau(d, t);
   }
 
   void timed_begin(int sweep, int it, cudaEvent_t* a) {
@@ -372,13 +410,9 @@ struct pcgpu_stepper {
     return 0;
   }
 
-  // State layout of the field between steps: N in exact mode (the radial
-  // sweep's explicit pass reads N and writes the T copies it needs), T in fast
-  // mode (the axial sweep's output layout; the radial explicit pass reads T).
-  bool fast() const { return d.mode == PCGPU_MODE_FAST; }
-
-  // Radial half-step from the anchor `field` (state layout). On success *res
-  // points at the result: T layout (exact) / N layout (fast).
+  // Radial half-step from the anchor `field` (N layout: the explicit pass
+  // reads N and writes the T copies the sweep needs). On success *res points
+  // at the result (T layout).
   int radial(const double* field, double t, double tau, const double** res, pcgpu_outcome* o) {
     const double pulse = pulse_for(t, tau);
     const double hk = 2.0 / tau;
@@ -387,20 +421,11 @@ struct pcgpu_stepper {
     auto src_of = [&](int it) -> const double* {
       return it == 1 ? buf[kTcT] : (it % 2 == 0 ? buf[kHalfT] : buf[kIterT]);
     };
-    int conv;
-    if (!fast()) {
-      launch_explicit_axial_exact(P, field, buf[kExpl], buf[kTcT], st, stream);
-      conv = picard(0, pred_radial, [&](int it) {
-        launch_radial_exact(P, it, d.epsilon, hk, pulse, src_of(it), buf[kTcT], buf[kExpl],
-                            buf[kPowT], dst_of(it), buf[kW], buf[kX], st, stream);
-      }, o);
-    } else {
-      launch_explicit_axial_fast(P, field, buf[kExpl], buf[kTcT], st, stream);
-      conv = picard(0, pred_radial, [&](int it) {
-        launch_radial_fast(P, it, d.epsilon, hk, pulse, src_of(it), buf[kTcT], buf[kExpl],
-                           buf[kPowN], dst_of(it), st, stream);
-      }, o);
-    }
+    launch_explicit_axial_exact(P, field, buf[kExpl], buf[kTcT], st, stream);
+    const int conv = picard(0, pred_radial, [&](int it) {
+      launch_radial_exact(P, it, d.epsilon, hk, pulse, src_of(it), buf[kTcT], buf[kExpl],
+                          buf[kPowT], dst_of(it), buf[kW], buf[kX], st, stream);
+    }, o);
     if (conv < 0) return -conv;
     if (conv > 0) *res = dst_of(conv);
     return PCGPU_OK;
@@ -552,53 +577,37 @@ struct pcgpu_stepper {
     return PCGPU_OK;
   }
 
-  // Axial half-step from the radial result `half` (T layout in exact mode, N
-  // in fast mode). `out` (state layout) is the preferred destination; *res
-  // receives the state-layout buffer holding the result (out or the
-  // ping-pong buffer).
+  // Axial half-step from the radial result `half` (T layout). `out` (N
+  // layout) is the preferred destination; *res receives the buffer holding
+  // the result (out or the ping-pong buffer).
   int axial(const double* half, double t, double tau, double* out, const double** res,
             pcgpu_outcome* o) {
     const double pulse = pulse_for(t, tau);
     const double hk = 2.0 / tau;
     reset_status();
-    double* anchor = buf[kTcT];  // halfN (exact) / halfT (fast)
+    double* anchor = buf[kTcT];  // halfN
     auto src_of = [&](int it) -> const double* {
       return it == 1 ? anchor : (it % 2 == 0 ? out : buf[kIterT]);
     };
     auto dst_of = [&](int it) -> double* { return it % 2 == 1 ? out : buf[kIterT]; };
-    int conv;
-    if (!fast()) {
-      // exact lookups: the axial sweep computes K-bar from T_half (no K-bar field)
-      double* kbar = kbar_on_the_fly(P) ? nullptr : buf[kKbar];
-      launch_axial_rhs_exact(P, hk, pulse, half, buf[kPowN], kbar, buf[kExpl], anchor, st, stream);
-      conv = picard(1, pred_axial, [&](int it) {
-        launch_axial_exact(P, it, d.epsilon, hk, src_of(it), anchor, kbar, buf[kExpl], dst_of(it),
-                           buf[kW], buf[kX], st, stream);
-      }, o);
-    } else {
-      launch_axial_rhs_fast(P, pulse, half, buf[kPowN], buf[kExpl], anchor, st, stream);
-      conv = picard(1, pred_axial, [&](int it) {
-        launch_axial_fast(P, it, d.epsilon, hk, src_of(it), anchor, buf[kExpl], dst_of(it), st,
-                          stream);
-      }, o);
-    }
+    // exact lookups: the axial sweep computes K-bar from T_half (no K-bar field)
+    double* kbar = kbar_on_the_fly(P) ? nullptr : buf[kKbar];
+    launch_axial_rhs_exact(P, hk, pulse, half, buf[kPowN], kbar, buf[kExpl], anchor, st, stream);
+    const int conv = picard(1, pred_axial, [&](int it) {
+      launch_axial_exact(P, it, d.epsilon, hk, src_of(it), anchor, kbar, buf[kExpl], dst_of(it),
+                         buf[kW], buf[kX], st, stream);
+    }, o);
     if (conv < 0) return -conv;
     if (conv > 0) *res = dst_of(conv);
     return PCGPU_OK;
   }
 
-  // N-layout user field <-> state layout.
+  // The user field and the resident state are both N layout.
   void to_state(const double* fieldN, double* state) {
-    if (fast())
-      launch_transpose_N2T(P, fieldN, state, stream);
-    else
-      CK(cudaMemcpyAsync(state, fieldN, sizeof(double) * cells(), cudaMemcpyDeviceToDevice,
-                         stream));
+    CK(cudaMemcpyAsync(state, fieldN, sizeof(double) * cells(), cudaMemcpyDeviceToDevice, stream));
   }
   void from_state(const double* state, double* fieldN) {
-    if (fast())
-      launch_transpose_T2N(P, state, fieldN, stream);
-    else if (state != fieldN)
+    if (state != fieldN)
       CK(cudaMemcpyAsync(fieldN, state, sizeof(double) * cells(), cudaMemcpyDeviceToDevice,
                          stream));
   }
@@ -607,7 +616,7 @@ struct pcgpu_stepper {
   // acceptance *accepted holds the N-layout buffer with the new field.
   int step(const double* field, double t, double* next, const double** accepted,
            pcgpu_step_result* r, double* attempt_updates, double tau0 = -1.0) {
-    double tau = tau0 > 0 ? tau0 : host_initial_tau(d, t);
+    double tau = tau0 > 0 ? tau0 : initial_tau(t);
     std::memset(r, 0, sizeof *r);
     const double* host = pipe_host;  // first attempt only
     pipe_host = nullptr;
@@ -641,15 +650,241 @@ struct pcgpu_stepper {
         char msg[160];
         std::snprintf(msg, sizeof msg, "time step %f fell below floor %f at t=%f", tau,
                       tau_floor, t);
+        fail_tau = tau;
+        fail_t = t;
         return fail(PCGPU_ERR_TAU_FLOOR, msg);
       }
       r->axial = pcgpu_outcome{};
     }
   }
+
+  // ---- resident stepper ------------------------------------------------------
+  bool res_ready() {
+    if (!res_grid) return false;
+    if (res_ctl) return true;
+    CK(cudaMalloc(&res_ctl, sizeof(ResCtl)));
+    dev_allocs.push_back(res_ctl);
+    CK(cudaMallocHost(&res_ctl_host, sizeof(ResCtl)));
+    CK(cudaMalloc(&res_sched, sizeof(ResSched) * kResBatch));
+    dev_allocs.push_back(res_sched);
+    CK(cudaMallocHost(&res_sched_host, sizeof(ResSched) * kResBatch));
+    CK(cudaMalloc(&res_log, sizeof(ResLog) * kResBatch));
+    dev_allocs.push_back(res_log);
+    CK(cudaMallocHost(&res_log_host, sizeof(ResLog) * kResBatch));
+    CK(cudaMalloc(&res_st2, sizeof(DevStatus) * 2));
+    dev_allocs.push_back(res_st2);
+    CK(cudaMalloc(&res_probe_off, sizeof(int) * kResProbes));
+    dev_allocs.push_back(res_probe_off);
+    return true;
+  }
+
+  // One schedule entry: the first attempt's tau and the pulse of every
+  // attempt (tau halved h times, exactly as step() halves it).
+  void res_entry(ResSched& e, double t, double tau0) const {
+    e.tau0 = tau0;
+    double tau = tau0;
+    for (int q = 0; q <= kResHalv; ++q) {
+      e.pulse[q] = pulse_for(t, tau);
+      tau *= 0.5;
+    }
+  }
+
+  // Runs res_sched_host[0..n) from field buffer X[state]; one host sync.
+  // Returns the control block (copied to res_ctl_host); the accepted steps'
+  // logs are in res_log_host[0..ctl.steps).
+  const ResCtl& res_batch(double* const X[3], int state, int n, int n_probes) {
+    ResArgs A{};
+    for (int q = 0; q < 3; ++q) A.X[q] = X[q];
+    A.TcT = buf[kTcT];
+    A.ExplT = buf[kExpl];
+    A.HalfT = buf[kHalfT];
+    A.kbarN = kbar_on_the_fly(P) ? nullptr : buf[kKbar];
+    A.W = buf[kW];
+    A.Xs = buf[kX];
+    A.st2 = res_st2;
+    A.sched = res_sched;
+    A.log = res_log;
+    A.ctl = res_ctl;
+    A.probe_off = res_probe_off;
+    A.n_probes = n_probes;
+    A.nsteps = n;
+    A.state0 = state;
+    A.max_iter = d.max_iter;
+    const char* mh = std::getenv("PCGPU_RES_MAX_HALV");  // test knob
+    A.max_halv = mh ? std::max(0, std::min(kResHalv, std::atoi(mh))) : kResHalv;
+    A.eps = d.epsilon;
+    A.profile = res_profile ? 1 : 0;
+    A.tau_floor = tau_floor;
+    A.active = static_cast<double>(active);
+    CK(cudaMemcpyAsync(res_sched, res_sched_host, sizeof(ResSched) * n, cudaMemcpyHostToDevice,
+                       stream));
+    if (res_profile) {
+      CK(cudaMemsetAsync(res_ctl->prof_ns, 0, sizeof(res_ctl->prof_ns), stream));
+      CK(cudaMemsetAsync(res_ctl->prof_n, 0, sizeof(res_ctl->prof_n), stream));
+    }
+    launch_resident(P, A, res_grid, stream);
+    CK(cudaMemcpyAsync(res_ctl_host, res_ctl, sizeof(ResCtl), cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(res_log_host, res_log, sizeof(ResLog) * n, cudaMemcpyDeviceToHost,
+                       stream));
+    CK(cudaStreamSynchronize(stream));
+    if (res_profile)
+      for (int q = 0; q < 8; ++q) {
+        res_prof_ns[q] += res_ctl_host->prof_ns[q];
+        res_prof_n[q] += res_ctl_host->prof_n[q];
+      }
+    ++res_batches;
+    res_steps += res_ctl_host->steps;
+    return *res_ctl_host;
+  }
+
+  // A batch's stop other than "ran" / "halved" as a status (field intact at
+  // X[ctl.state]): line error, tau floor. t = the failed step's time.
+  int res_fail(const ResCtl& c, double t) {
+    if (c.stop == kResError) {
+      st_host->err = c.err;
+      return check_line_error();
+    }
+    char msg[160];
+    std::snprintf(msg, sizeof msg, "time step %f fell below floor %f at t=%f", c.tau, tau_floor, t);
+    fail_tau = c.tau;
+    fail_t = t;
+    return fail(PCGPU_ERR_TAU_FLOOR, msg);
+  }
+
+  // The step the batch could not finish (more than kResHalv halvings) on the
+  // host-driven path, from X[*state]; rotates *state. Same arithmetic, same bits.
+  int res_host_step(double* const X[3], int* state, double t, double tau0,
+                    pcgpu_step_result* r, double* upd) {
+    const int s = *state;
+    double* saved = buf[kIterT];
+    buf[kIterT] = X[(s + 2) % 3];
+    const double* acc = nullptr;
+    const int rc = step(X[s], t, X[(s + 1) % 3], &acc, r, upd, tau0);
+    buf[kIterT] = saved;
+    ++res_host_steps;
+    if (rc) return rc;
+    *state = acc == X[(s + 1) % 3] ? (s + 1) % 3 : (s + 2) % 3;
+    return PCGPU_OK;
+  }
+
+  // Controller above the resident batches. `next_tau(t, k)` gives the first
+  // attempt's tau of step k (scheduled with no halvings before it);
+  // `accept(r)` updates the controller with an accepted step's result and
+  // returns false to stop. Stops after max_steps or when `more(t)` is false.
+  template <typename Plan, typename Accept, typename More>
+  int res_run(double* const X[3], int* state, double* t, int64_t max_steps, Plan&& plan,
+              Accept&& accept, More&& more, pcgpu_step_result* results, pcgpu_run_stats* s,
+              int n_probes = 0, const std::function<bool(int64_t, const ResLog&)>& on_log = {}) {
+    res_ready();
+    int64_t done = 0;
+    while (done < max_steps && more(*t)) {
+      // speculate: no halvings in the batch
+      int n = 0;
+      double tt = *t;
+      typename std::decay<decltype(plan.state())>::type ps = plan.state();
+      while (n < kResBatch && done + n < max_steps && (n == 0 || more(tt))) {
+        const double tau0 = plan.next(ps, tt);
+        res_entry(res_sched_host[n], tt, tau0);
+        plan.advance(ps, tau0);
+        tt += tau0;
+        ++n;
+      }
+      const ResCtl& c = res_batch(X, *state, n, n_probes);
+      for (int q = 0; q < c.steps; ++q) {
+        const ResLog& lg = res_log_host[q];
+        const pcgpu_step_result& r = lg.r;
+        *t += r.tau_used;
+        if (results) results[done] = r;
+        s->steps += 1;
+        s->halvings += r.halvings;
+        s->radial_iterations += r.radial.iterations;
+        s->axial_iterations += r.axial.iterations;
+        s->cell_updates += lg.updates;
+        s->cell_updates_accepted +=
+            static_cast<double>(active) * (r.radial.iterations + r.axial.iterations);
+        s->attempt_cells += 2.0 * static_cast<double>(active) * (r.halvings + 1);
+        accept(r);
+        ++done;
+        if (on_log && !on_log(done, lg)) {
+          *state = c.state;
+          return PCGPU_OK;
+        }
+      }
+      *state = c.state;
+      if (c.stop == kResError || c.stop == kResFloor) return res_fail(c, *t);
+      if (c.stop == kResNeedHost) {
+        pcgpu_step_result r;
+        double upd = 0;
+        const double tau0 = plan.next(plan.state(), *t);
+        const int rc = res_host_step(X, state, *t, tau0, &r, &upd);
+        s->cell_updates += upd;
+        if (rc) return rc;
+        *t += r.tau_used;
+        if (results) results[done] = r;
+        s->steps += 1;
+        s->halvings += r.halvings;
+        s->radial_iterations += r.radial.iterations;
+        s->axial_iterations += r.axial.iterations;
+        s->cell_updates_accepted +=
+            static_cast<double>(active) * (r.radial.iterations + r.axial.iterations);
+        s->attempt_cells += 2.0 * static_cast<double>(active) * (r.halvings + 1);
+        accept(r);
+        ++done;
+        if (on_log) {
+          ResLog lg{};
+          lg.r = r;
+          lg.updates = upd;
+          gather_probes_host(X[*state], n_probes, lg.probes);
+          if (!on_log(done, lg)) return PCGPU_OK;
+        }
+      }
+    }
+    return PCGPU_OK;
+  }
+
+  void gather_probes_host(const double* field, int n, double* out) {
+    if (n <= 0) return;
+    std::vector<int> off(n);
+    CK(cudaMemcpy(off.data(), res_probe_off, sizeof(int) * n, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < n; ++k)
+      CK(cudaMemcpyAsync(out + k, field + off[k], sizeof(double), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+  }
+  double fail_tau = 0, fail_t = 0;
 };
 
-// DevProblem from the descriptor: metric reciprocals, flattened tables and
-// the fast-mode table forms, uploaded to the current device. Shared by the
+// Schedules for the resident stepper's controller (pcgpu_stepper::res_run).
+// A plan gives the first attempt's tau of the next step from its state and
+// advances the state as if the step were accepted without halving.
+struct FixedPlan {  // step(): tau = initial_tau(t) every step (solver.cpp:357)
+  const pcgpu_stepper* h;
+  struct State {};
+  State state() const { return {}; }
+  double next(const State&, double t) const { return h->initial_tau(t); }
+  void advance(State&, double) const {}
+};
+struct GrowthPlan {  // the BASELINE growth policy (pcgpu_run_growth)
+  double grow, tau_max;
+  int easy_steps;
+  struct State {
+    double tau;
+    int easy;
+  } st;
+  State state() const { return st; }
+  double next(const State& s, double) const { return s.tau; }
+  void advance(State& s, double tau_used) const { update(s, tau_used, 0); }
+  void update(State& s, double tau_used, int halvings) const {
+    s.tau = tau_used;
+    s.easy = halvings == 0 ? s.easy + 1 : 0;
+    if (s.easy >= easy_steps) {
+      s.tau = std::min(s.tau * grow, tau_max);
+      s.easy = 0;
+    }
+  }
+};
+
+// DevProblem from the descriptor: metric reciprocals and flattened tables,
+// uploaded to the current device. Shared by the
 // single-GPU stepper and the partitioned (multi-GPU) stepper.
 void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& allocs) {
   const int nr = d->nr, nz = d->nz;
@@ -676,7 +911,7 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
     std::vector<int> layer(d->layer, d->layer + nr);
 
     // Tables, flattened.
-    std::vector<double> knots, vals, slopes, ivl, xpair;
+    std::vector<double> knots, vals, xpair;
     
     P.n_layers = d->n_layers;
     for (int m = 0; m < d->n_layers; ++m) {
@@ -692,13 +927,6 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
         for (int k = 0; k < t.n; ++k) {
           knots.push_back(t.t[k]);
           vals.push_back(t.v[k]);
-          const double sl = k == 0 ? 0.0 : (t.v[k] - t.v[k - 1]) / (t.t[k] - t.t[k - 1]);
-          slopes.push_back(sl);
-          // packed interval k: {t[k-1], t[k], v[k-1], slope_k}
-          ivl.push_back(k == 0 ? t.t[0] : t.t[k - 1]);
-          ivl.push_back(t.t[k]);
-          ivl.push_back(k == 0 ? t.v[0] : t.v[k - 1]);
-          ivl.push_back(sl);
           xpair.push_back(t.v[k]);
           xpair.push_back(k + 1 < t.n ? t.v[k + 1] - t.v[k] : 0.0);
         }
@@ -741,30 +969,6 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
         }
       }
     }
-    P.all_u2 = 1;
-    for (int m = 0; m < d->n_layers; ++m)
-      for (int p = 0; p < 3; ++p)
-        if (P.mats[m].n[p] > 0 && P.mats[m].uniform[p] != 2) P.all_u2 = 0;
-    // Lean fast kernels: MeanTemperature faces, Clamp policy, Joule/Null
-    // source, every table exactly uniform and one knot grid per property.
-    P.lean = P.all_u2 && d->halfpoint_rule == PCGPU_HALFPOINT_MEAN_TEMPERATURE &&
-             d->range_policy == PCGPU_RANGE_CLAMP && d->source_kind != PCGPU_SOURCE_FIELD;
-    for (int p = 0; p < 3 && P.lean; ++p) {
-      int ref = -1;
-      for (int m = 0; m < d->n_layers; ++m) {
-        if (P.mats[m].n[p] == 0) {
-          if (p < 2) P.lean = 0;  // cv / lambda are mandatory
-          continue;
-        }
-        if (ref < 0) { ref = m; continue; }
-        const DevMaterial &a = P.mats[ref], &b = P.mats[m];
-        if (a.n[p] != b.n[p] || a.t_first[p] != b.t_first[p] || a.t_last[p] != b.t_last[p] ||
-            a.inv_h[p] != b.inv_h[p])
-          P.lean = 0;
-      }
-    }
-    if (d->source_kind == PCGPU_SOURCE_JOULE && P.mats[d->source_layer].n[2] == 0) P.lean = 0;
-    if (std::getenv("PCGPU_NO_LEAN")) P.lean = 0;
     // exact kernels' branch-free lookups: lambda/cv tables xmode 1 whose t0 >= 0
     // is a multiple of h and whose top knot's ulp is below h (T - t0 exact), chi
     // a single interval or absent; MeanTemperature faces.
@@ -832,48 +1036,6 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
     P.exact_ws = std::getenv("PCGPU_NO_EXACTWS") ? 0 : 1;
     // test knob: every full tile of the line solvers takes the reciprocal redo path
     P.rcp_redo = std::getenv("PCGPU_RCP_REDO") ? 1 : 0;
-    std::vector<double> lt, lab;  // lean tables, uploaded below
-    if (P.lean) {
-      // property-grouped lean table: (prop, layer, k) -> {v[k-1], slope_k}
-      for (int p = 0; p < 3; ++p) {
-        int ref = -1;
-        for (int m = 0; m < d->n_layers; ++m)
-          if (P.mats[m].n[p] > 0) { ref = m; break; }
-        const int n = ref >= 0 ? P.mats[ref].n[p] : 1;
-        P.lean_base[p] = static_cast<int>(lt.size() / 2);
-        P.lean_stride[p] = n;
-        P.lean_kmax[p] = n - 1 < 1 ? 1 : n - 1;
-        P.lean_t0[p] = ref >= 0 ? P.mats[ref].t_first[p] : 0.0;
-        P.lean_tK[p] = ref >= 0 ? P.mats[ref].t_last[p] : 0.0;
-        P.lean_inv_h[p] = ref >= 0 ? P.mats[ref].inv_h[p] : 0.0;
-        P.lean_h[p] = P.lean_inv_h[p] > 0.0 ? 1.0 / P.lean_inv_h[p] : 0.0;
-        if (ref >= 0) {
-          const double t0 = P.mats[ref].t_first[p], tK = P.mats[ref].t_last[p];
-          P.lean_ih[p] = (n - 1) / (tK - t0);
-          P.lean_x0[p] = t0 * P.lean_ih[p];
-          P.lean_kmaxd[p] = n - 1;
-        }
-        for (int m = 0; m < d->n_layers; ++m) {
-          const double scale = p == 0 ? d->materials[m].rho : 1.0;  // rho folded into c_V
-          for (int k = 0; k < n; ++k) {
-            if (P.mats[m].n[p] == n && k >= 1) {
-              const int o = P.mats[m].off[p] + k;
-              lt.push_back(vals[o - 1]);
-              lt.push_back(slopes[o]);
-              const double sl = slopes[o];
-              lab.push_back(scale * (vals[o - 1] - sl * knots[o - 1]));
-              lab.push_back(scale * sl);
-            } else {
-              lt.push_back(0.0);
-              lt.push_back(0.0);
-              lab.push_back(0.0);
-              lab.push_back(0.0);
-            }
-          }
-        }
-      }
-      for (int m = 0; m < d->n_layers; ++m) P.lean_rho[m] = d->materials[m].rho;
-    }
     P.nr = nr;
     P.nz = nz;
     P.nr_core = d->nr_core;
@@ -912,23 +1074,6 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
     P.width_z = up(width_z);
     P.knots = up(knots);
     P.vals = up(vals);
-    P.slopes = up(slopes);
-    if (P.lean) {
-      P.lean_tab = up(lt);
-      P.lean_ab = up(lab);
-      std::vector<double> rm(2 * static_cast<size_t>(nr)), zm(2 * static_cast<size_t>(nz));
-      for (int i = 0; i < nr; ++i) {
-        rm[2 * i] = i + 1 < nr ? face_r_lo[i + 1] * inv_gap_r[i + 1] : 0.0;
-        rm[2 * i + 1] = inv_vol_r[i];
-      }
-      for (int j = 0; j < nz; ++j) {
-        zm[2 * j] = inv_gap_z[j + 1];
-        zm[2 * j + 1] = inv_eta[j];
-      }
-      P.rmet = up(rm);
-      P.zmet = up(zm);
-    }
-    P.ivl = up(ivl);
     P.xpair = up(xpair);
     if (P.exact_lean) P.xe_tab = up(xe);
     P.source_kind = d->source_kind;
@@ -960,12 +1105,37 @@ std::string pcgpu_validate_desc(const pcgpu_desc* d) { return validate(d); }
 double pcgpu_host_initial_tau(const pcgpu_desc& d, double t) { return host_initial_tau(d, t); }
 double pcgpu_host_pulse_value(const pcgpu_desc& d, double t) { return host_pulse_value(d, t); }
 
-#define GUARD_BEGIN try {
+#define GUARD_BEGIN DeviceGuard dg_(h->d.device); try {
 #define GUARD_END(h)                                                                  \
   }                                                                                   \
   catch (const CudaError& ce) {                                                       \
     return (h)->fail(PCGPU_ERR_CUDA, std::string(ce.what) + ": " + cudaGetErrorString(ce.e)); \
   }
+
+// Steps bound a FIELD source's power per half-step (the caller binds it
+// before every half-step); the whole-step entry points cannot.
+static int reject_field_source(pcgpu_stepper* h) {
+  if (h->d.source_kind != PCGPU_SOURCE_FIELD) return PCGPU_OK;
+  return h->fail(PCGPU_ERR_CONFIG,
+                 "a FIELD source is bound per half-step (pcgpu_bind_power_field): drive "
+                 "radial_half_step / axial_half_step instead of step / run / evolve");
+}
+
+// The resident stepper on the rotation X = {field buffer, next, spare}; the
+// field enters X[0] and leaves X[state]; the stepper's buffer roles follow.
+template <typename Run>
+static int resident_run(pcgpu_stepper* h, double* field, Run&& run) {
+  double* X[3] = {h->buf[kField], h->buf[kNext], h->buf[kIterT]};
+  h->to_state(field, X[0]);
+  int state = 0;
+  const int rc = run(X, &state);
+  h->from_state(X[state], field);
+  h->buf[kField] = X[state];
+  h->buf[kNext] = X[(state + 1) % 3];
+  h->buf[kIterT] = X[(state + 2) % 3];
+  CK(cudaStreamSynchronize(h->stream));
+  return rc;
+}
 
 extern "C" {
 
@@ -986,10 +1156,14 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
     g_create_error = v;
     return PCGPU_ERR_CONFIG;
   }
+  DeviceGuard dg(d->device);
+  if (!dg.ok) {
+    g_create_error = "pcgpu_create: cannot select device " + std::to_string(d->device);
+    return PCGPU_ERR_CUDA;
+  }
   auto h = std::make_unique<pcgpu_stepper>();
   try {
     h->d = *d;
-    CK(cudaSetDevice(d->device));
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     const int nr = d->nr, nz = d->nz;
     h->tau_floor = d->tau_min > 0 ? d->tau_min : 1e-12 * d->t_per;  // solver.hpp:28-30
@@ -1012,16 +1186,21 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
     std::vector<double> t0fill(h->cells(), d->T0);
     for (int b = 0; b < kNumBufs; ++b) {
       if ((b == kPowN || b == kPowT) && d->source_kind != PCGPU_SOURCE_FIELD) continue;
-      if ((b == kW || b == kKbar) && d->mode == PCGPU_MODE_FAST) continue;  // exact-mode only
       if (b == kKbar && kbar_on_the_fly(h->P)) continue;  // computed inside the axial sweep
       if (b == kStage) continue;  // lazily, by the *_host entry points
       double* p = nullptr;
       CK(cudaMalloc(&p, bytes));
       h->dev_allocs.push_back(p);
-      CK(cudaMemcpy(p, t0fill.data(), bytes, cudaMemcpyHostToDevice));
+      if (b == kPowN || b == kPowT)  // no power until pcgpu_bind_power_field
+        CK(cudaMemset(p, 0, bytes));
+      else
+        CK(cudaMemcpy(p, t0fill.data(), bytes, cudaMemcpyHostToDevice));
       h->buf[b] = p;
     }
     CK(cudaDeviceSynchronize());
+    // the resident stepper where it applies ($PCGPU_RESIDENT=0: host-driven steps)
+    const char* rv = std::getenv("PCGPU_RESIDENT");
+    h->res_grid = (rv && std::atoi(rv) == 0) ? 0 : resident_grid(h->P);
     h->launches0 = g_launches;
   } catch (const CudaError& ce) {
     g_create_error = std::string(ce.what) + ": " + cudaGetErrorString(ce.e);
@@ -1031,7 +1210,11 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
   return PCGPU_OK;
 }
 
-void pcgpu_destroy(pcgpu_stepper* h) { delete h; }
+void pcgpu_destroy(pcgpu_stepper* h) {
+  if (!h) return;
+  DeviceGuard dg(h->d.device);
+  delete h;
+}
 
 const char* pcgpu_last_error(const pcgpu_stepper* h) {
   return h ? h->err.c_str() : g_create_error.c_str();
@@ -1039,9 +1222,38 @@ const char* pcgpu_last_error(const pcgpu_stepper* h) {
 
 int64_t pcgpu_error_line(const pcgpu_stepper* h) { return h ? h->err_line : -1; }
 
-double pcgpu_initial_tau(const pcgpu_stepper* h, double t) { return host_initial_tau(h->d, t); }
-double pcgpu_pulse_value(const pcgpu_stepper* h, double t) { return host_pulse_value(h->d, t); }
+double pcgpu_initial_tau(const pcgpu_stepper* h, double t) { return h->initial_tau(t); }
+double pcgpu_pulse_value(const pcgpu_stepper* h, double t) {
+  return h->pulse_fn ? h->pulse_fn(h->clock_user, t) : host_pulse_value(h->d, t);
+}
 int64_t pcgpu_active_cells(const pcgpu_stepper* h) { return h->active; }
+
+int pcgpu_set_host_clock(pcgpu_stepper* h, pcgpu_clock_fn pulse_value, pcgpu_clock_fn initial_tau,
+                         void* user) {
+  if (!h) return PCGPU_ERR_ARG;
+  h->pulse_fn = pulse_value;
+  h->tau_fn = initial_tau;
+  h->clock_user = user;
+  return PCGPU_OK;
+}
+
+int pcgpu_last_tau_floor(const pcgpu_stepper* h, double* tau, double* floor, double* t) {
+  if (!h || !tau || !floor || !t) return PCGPU_ERR_ARG;
+  *tau = h->fail_tau;
+  *floor = h->tau_floor;
+  *t = h->fail_t;
+  return PCGPU_OK;
+}
+
+int pcgpu_resident_stats(const pcgpu_stepper* h, int32_t* grid, int64_t* batches, int64_t* steps,
+                         int64_t* host_steps) {
+  if (!h || !grid || !batches || !steps || !host_steps) return PCGPU_ERR_ARG;
+  *grid = h->res_grid;
+  *batches = h->res_batches;
+  *steps = h->res_steps;
+  *host_steps = h->res_host_steps;
+  return PCGPU_OK;
+}
 void* pcgpu_stream(const pcgpu_stepper* h) { return h->stream; }
 int64_t pcgpu_launch_count(const pcgpu_stepper* h) {
   return static_cast<int64_t>(g_launches - h->launches0);
@@ -1049,15 +1261,10 @@ int64_t pcgpu_launch_count(const pcgpu_stepper* h) {
 
 int32_t pcgpu_describe(const pcgpu_stepper* h, char* buf, int32_t len) {
   std::string s;
-  if (h->d.mode == PCGPU_MODE_EXACT) {
-    s = "mode=exact lines=";
-    s += h->P.exact_ws ? "ws" : "thread";
-    s += " lookups=";
-    s += h->P.exact_lean ? "exact-lean" : (h->P.exact_x ? "exact-x" : "generic");
-  } else {
-    s = "mode=fast lookups=";
-    s += h->P.lean ? "lean" : (h->P.all_u2 ? "u2" : "generic");
-  }
+  s = "mode=exact lines=";
+  s += h->P.exact_ws ? "ws" : "thread";
+  s += " lookups=";
+  s += h->P.exact_lean ? "exact-lean" : (h->P.exact_x ? "exact-x" : "generic");
   if (buf && len > 0) {
     const size_t n = std::min(s.size(), static_cast<size_t>(len - 1));
     std::memcpy(buf, s.data(), n);
@@ -1078,25 +1285,27 @@ int pcgpu_bind_power_field(pcgpu_stepper* h, const double* power_dev) {
   return PCGPU_OK;
 }
 
+// A FIELD source's power array is bound for one half-step at a time (the
+// reference binds the source's time inside every half-step, solver.cpp:238,
+// :337): each half-step consumes the binding.
+static int consume_power_binding(pcgpu_stepper* h) {
+  if (h->d.source_kind != PCGPU_SOURCE_FIELD) return PCGPU_OK;
+  if (!h->power_bound)
+    return h->fail(PCGPU_ERR_CONFIG,
+                   "FIELD source: pcgpu_bind_power_field must precede every half-step");
+  h->power_bound = false;
+  return PCGPU_OK;
+}
+
 int pcgpu_radial_half_step(pcgpu_stepper* h, const double* T_cur, double t, double tau,
                            double* out, pcgpu_outcome* o) {
   if (!h || !T_cur || !out || !o || out == T_cur) return PCGPU_ERR_ARG;
+  if (const int e = consume_power_binding(h)) return e;
   GUARD_BEGIN
-  const double* anchor = T_cur;
-  if (h->fast()) {
-    launch_transpose_N2T(h->P, T_cur, h->buf[kX], h->stream);
-    anchor = h->buf[kX];
-  }
   const double* res = nullptr;
-  const int rc = h->radial(anchor, t, tau, &res, o);
+  const int rc = h->radial(T_cur, t, tau, &res, o);
   if (rc) return rc;
-  if (o->converged) {
-    if (!h->fast())
-      launch_transpose_T2N(h->P, res, out, h->stream);
-    else
-      CK(cudaMemcpyAsync(out, res, sizeof(double) * h->cells(), cudaMemcpyDeviceToDevice,
-                         h->stream));
-  }
+  if (o->converged) launch_transpose_T2N(h->P, res, out, h->stream);
   CK(cudaStreamSynchronize(h->stream));
   GUARD_END(h)
   return PCGPU_OK;
@@ -1105,15 +1314,11 @@ int pcgpu_radial_half_step(pcgpu_stepper* h, const double* T_cur, double t, doub
 int pcgpu_axial_half_step(pcgpu_stepper* h, const double* T_half, double t, double tau,
                           double* out, pcgpu_outcome* o) {
   if (!h || !T_half || !out || !o || out == T_half) return PCGPU_ERR_ARG;
+  if (const int e = consume_power_binding(h)) return e;
   GUARD_BEGIN
-  const double* half = T_half;
-  if (!h->fast()) {
-    launch_transpose_N2T(h->P, T_half, h->buf[kHalfT], h->stream);
-    half = h->buf[kHalfT];
-  }
-  double* dst = h->fast() ? h->buf[kNext] : out;
+  launch_transpose_N2T(h->P, T_half, h->buf[kHalfT], h->stream);
   const double* res = nullptr;
-  const int rc = h->axial(half, t, tau, dst, &res, o);
+  const int rc = h->axial(h->buf[kHalfT], t, tau, out, &res, o);
   if (rc) return rc;
   if (o->converged) h->from_state(res, out);
   CK(cudaStreamSynchronize(h->stream));
@@ -1123,15 +1328,34 @@ int pcgpu_axial_half_step(pcgpu_stepper* h, const double* T_half, double t, doub
 
 int pcgpu_step(pcgpu_stepper* h, double* field, double t, pcgpu_step_result* r) {
   if (!h || !field || !r) return PCGPU_ERR_ARG;
+  if (const int e = reject_field_source(h)) return e;
+  if (h->res_grid) {
+    // one resident step on X = {field, next, spare}; the result is copied into
+    // the caller's array (field.swap(next_), solver.cpp:364)
+    GUARD_BEGIN
+    double* X[3] = {field, h->buf[kNext], h->buf[kIterT]};
+    int state = 0;
+    double tt = t;
+    pcgpu_run_stats s{};
+    *r = pcgpu_step_result{};
+    const int rc = h->res_run(X, &state, &tt, 1, FixedPlan{h}, [](const pcgpu_step_result&) {},
+                              [](double) { return true; }, r, &s);
+    if (rc) return rc;
+    if (state != 0) {
+      CK(cudaMemcpyAsync(field, X[state], sizeof(double) * h->cells(), cudaMemcpyDeviceToDevice,
+                         h->stream));
+      // keep the three roles distinct: the other buffer stays the spare
+      h->buf[kNext] = X[state];
+      h->buf[kIterT] = X[state == 1 ? 2 : 1];
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    GUARD_END(h)
+    return PCGPU_OK;
+  }
   GUARD_BEGIN
   const double* acc = nullptr;
   double upd = 0;
-  const double* state = field;
-  if (h->fast()) {
-    h->to_state(field, h->buf[kField]);
-    state = h->buf[kField];
-  }
-  const int rc = h->step(state, t, h->buf[kNext], &acc, r, &upd);
+  const int rc = h->step(field, t, h->buf[kNext], &acc, r, &upd);
   if (rc) return rc;
   // field.swap(next_) (solver.cpp:364): the caller's array receives the result.
   h->from_state(acc, field);
@@ -1143,9 +1367,21 @@ int pcgpu_step(pcgpu_stepper* h, double* field, double t, pcgpu_step_result* r) 
 int pcgpu_run(pcgpu_stepper* h, double* field, double t0, int32_t nsteps,
               pcgpu_step_result* results, pcgpu_run_stats* stats) {
   if (!h || !field || nsteps < 0) return PCGPU_ERR_ARG;
+  if (const int e = reject_field_source(h)) return e;
   pcgpu_run_stats s{};
   double t = t0;
   int rc = PCGPU_OK;
+  if (h->res_grid) {
+    GUARD_BEGIN
+    rc = resident_run(h, field, [&](double* const X[3], int* state) {
+      return h->res_run(X, state, &t, nsteps, FixedPlan{h}, [](const pcgpu_step_result&) {},
+                        [](double) { return true; }, results, &s);
+    });
+    GUARD_END(h)
+    s.t_end = t;
+    if (stats) *stats = s;
+    return rc;
+  }
   GUARD_BEGIN
   // Resident field: rotate buffer roles instead of copying per step.
   double* cur = h->buf[kField];
@@ -1201,9 +1437,24 @@ int pcgpu_run_growth(pcgpu_stepper* h, double* field, double t0, double t_end, i
                      double tau_start, double grow, int32_t easy_steps, double tau_max,
                      pcgpu_step_result* results, pcgpu_run_stats* stats) {
   if (!h || !field || max_steps < 0 || !(tau_start > 0) || !(grow >= 1.0)) return PCGPU_ERR_ARG;
+  if (const int e = reject_field_source(h)) return e;
   pcgpu_run_stats s{};
   double t = t0, tau = std::min(tau_start, tau_max);
   int easy = 0, rc = PCGPU_OK;
+  if (h->res_grid) {
+    GUARD_BEGIN
+    GrowthPlan plan{grow, tau_max, easy_steps, {tau, 0}};
+    rc = resident_run(h, field, [&](double* const X[3], int* state) {
+      return h->res_run(
+          X, state, &t, max_steps, plan,
+          [&](const pcgpu_step_result& r) { plan.update(plan.st, r.tau_used, r.halvings); },
+          [&](double tt) { return tt < t_end; }, results, &s);
+    });
+    GUARD_END(h)
+    s.t_end = t;
+    if (stats) *stats = s;
+    return rc;
+  }
   GUARD_BEGIN
   double* cur = h->buf[kField];
   double* nxt = h->buf[kNext];
@@ -1273,7 +1524,7 @@ int pcgpu_step_host(pcgpu_stepper* h, double* field_host, double t, pcgpu_step_r
   const bool no_pipe = std::getenv("PCGPU_NO_PIPELINE") != nullptr;
   const char* mv = std::getenv("PCGPU_PIPELINE_MIN_NZ");  // tests: pipeline small grids
   const int min_nz = mv ? std::atoi(mv) : 2048;
-  if (!h->fast() && h->P.exact_ws && !no_pipe && h->d.nz >= min_nz) {
+  if (h->P.exact_ws && !no_pipe && h->d.nz >= min_nz && !h->res_grid) {
     // the copy-in overlaps K3 and the first radial iterations (radial_pipelined);
     // the accepted buffer goes straight back to the host
     const double* acc = nullptr;
@@ -1332,6 +1583,7 @@ int pcgpu_axial_half_step_host(pcgpu_stepper* h, const double* T_half_host, doub
 
 int pcgpu_clamp_events(const pcgpu_stepper* h, uint64_t* counts) {
   if (!h || !counts) return PCGPU_ERR_ARG;
+  DeviceGuard dg(h->d.device);
   if (cudaStreamSynchronize(h->stream) != cudaSuccess) return PCGPU_ERR_CUDA;
   if (cudaMemcpy(counts, h->P.clamp, sizeof(uint64_t) * h->d.n_layers, cudaMemcpyDeviceToHost) !=
       cudaSuccess)
@@ -1442,6 +1694,7 @@ int pcgpu_evolve(pcgpu_stepper* h, double* field, const pcgpu_runner_cfg* cfg,
                  pcgpu_step_cb on_step, pcgpu_snapshot_cb on_snapshot, void* user,
                  pcgpu_evolve_result* res) {
   if (!h || !field || !cfg || !res) return PCGPU_ERR_ARG;
+  if (const int e = reject_field_source(h)) return e;
   // RunnerConfig::validate (runner.hpp:96-102)
   if (!(cfg->t_end > 0)) return h->fail(PCGPU_ERR_CONFIG, "runner.t_end: must be > 0");
   if (cfg->detector_samples_per_period < 1)
@@ -1462,7 +1715,7 @@ int pcgpu_evolve(pcgpu_stepper* h, double* field, const pcgpu_runner_cfg* cfg,
     const int i = cfg->probe_i[k], j = cfg->probe_j[k];
     const bool in_mask = i >= 0 && i < d.nr && j >= 0 && j < h->col_ext_host[i];
     if (!in_mask) return h->fail(PCGPU_ERR_CONFIG, "probe cell falls outside the domain");
-    off[k] = h->fast() ? i * d.nz + j : j * d.nr + i;  // state layout
+    off[k] = j * d.nr + i;
   }
   *res = pcgpu_evolve_result{};
   res->fire_t = -1;
@@ -1484,76 +1737,62 @@ int pcgpu_evolve(pcgpu_stepper* h, double* field, const pcgpu_runner_cfg* cfg,
     }
   } free_guard{d_off, d_vals, h_vals};
   if (np) CK(cudaMemcpy(d_off, off.data(), sizeof(int) * np, cudaMemcpyHostToDevice));
-  double* cur = h->buf[kField];
-  double* nxt = h->buf[kNext];
-  double* spare = h->buf[kIterT];
-  h->to_state(field, cur);
-  auto probes = [&](const double* state) {
+  const bool resident = h->res_grid && np <= kResProbes && h->res_ready();
+  if (resident && np)
+    CK(cudaMemcpy(h->res_probe_off, off.data(), sizeof(int) * np, cudaMemcpyHostToDevice));
+  // field rotation X[state] (resident) / cur, nxt, spare (host-driven steps)
+  double* X[3] = {h->buf[kField], h->buf[kNext], h->buf[kIterT]};
+  int state = 0;
+  h->to_state(field, X[0]);
+  auto gather = [&](const double* f) {  // probe values of field f into h_vals
     if (!np) return;
-    k_gather_probes<<<1, 1024, 0, h->stream>>>(state, d_off, np, d_vals);
+    k_gather_probes<<<1, 1024, 0, h->stream>>>(f, d_off, np, d_vals);
     ++g_launches;
     CK(cudaMemcpyAsync(h_vals, d_vals, sizeof(double) * np, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
   };
-  // snapshots leave through the user layout (N): the state itself in exact
-  // mode, a transposed copy in fast mode
-  auto snapshot = [&](int kind, double ts, const double* state) {
+  auto snapshot = [&](int kind, double ts, const double* f) {  // N layout, device
     if (!on_snapshot) return;
-    const double* f = state;
-    if (h->fast()) {
-      ensure_stage(h);
-      h->from_state(state, h->buf[kStage]);
-      f = h->buf[kStage];
-    }
+    if (!f) throw CudaError{cudaErrorUnknown, "evolve: snapshot inside a multi-step batch"};
     CK(cudaStreamSynchronize(h->stream));
     on_snapshot(user, kind, ts, f);
   };
+  // Regime detection over probe 0: the caller's detector (e.g. the
+  // reference's own RegimeDetector through the C++ drop-in) or the
+  // restatement of runner.cpp:35-95 below.
   const bool detect = cfg->source_on && np > 0;
   RegimeDetectorGpu det(d.t_per, cfg->detector_samples_per_period, cfg->detector_tolerance,
                         cfg->detector_min_periods);
+  auto det_seed = [&](double t, double v) {
+    if (cfg->detect) cfg->detect(cfg->detect_user, 1, t, v);
+    else det.rs.seed(t, v);
+  };
+  auto det_update = [&](double t, double v) {
+    return cfg->detect ? cfg->detect(cfg->detect_user, 0, t, v) != 0 : det.update(t, v);
+  };
   if (detect) {
-    probes(cur);
-    det.rs.seed(0.0, h_vals[0]);
+    gather(X[0]);
+    det_seed(0.0, h_vals[0]);
   }
   long period_idx = 1, off_idx = 0;
   const double off_offset = d.t_src + d.t_trs;
   size_t next_time = 0;
   double t = 0, comp = 0;
   int stop = PCGPU_STOP_REACHED_TIME;
-  for (;;) {
-    if (t >= cfg->t_end) {
-      stop = PCGPU_STOP_REACHED_TIME;
-      break;
-    }
+  // The reference's per-step bookkeeping (runner.cpp:140-180) for an accepted
+  // step from field `prev` to field `cur` with probe values `vals`. Returns
+  // true when the regime detector fired.
+  auto after_step = [&](const pcgpu_step_result& r, const double* prev, const double* cur,
+                        const double* vals) {
     const double t_before = t;
-    pcgpu_step_result r;
-    const double* acc = nullptr;
-    double upd = 0;
-    h->buf[kIterT] = spare;
-    const int rc = h->step(cur, t, nxt, &acc, &r, &upd);
-    if (rc == PCGPU_ERR_TAU_FLOOR) {  // the field stays the last accepted one
-      stop = PCGPU_STOP_TAU_FLOOR;
-      break;
-    }
-    if (rc) {
-      h->buf[kField] = cur;
-      h->buf[kNext] = nxt;
-      h->buf[kIterT] = spare;
-      return rc;
-    }
-    // Kahan accumulation of the accepted steps (runner.cpp:141-146)
-    {
+    {  // Kahan accumulation of the accepted steps (runner.cpp:141-146)
       const double y = r.tau_used - comp;
       const double tt = t + y;
       comp = (tt - t) - y;
       t = tt;
     }
     res->steps += 1;
-    double* prev = cur;  // the step's input stays intact until the next step
-    cur = const_cast<double*>(acc);
-    if (cur == nxt) nxt = prev; else spare = prev;
-    probes(cur);
-    if (on_step) on_step(user, res->steps, t, r.tau_used, h_vals);
+    if (on_step) on_step(user, res->steps, t, r.tau_used, vals);
     const double edge = static_cast<double>(period_idx) * d.t_per;
     if (cfg->snapshot_pre_on && t >= edge && t_before < edge)
       snapshot(PCGPU_SNAP_PRE_ON, t_before, prev);
@@ -1566,21 +1805,127 @@ int pcgpu_evolve(pcgpu_stepper* h, double* field, const pcgpu_runner_cfg* cfg,
       snapshot(PCGPU_SNAP_AT_TIME, t, cur);
       ++next_time;
     }
-    if (detect && det.update(t, h_vals[0])) {
+    if (detect && det_update(t, vals[0])) {
       res->fire_t = t;
       stop = PCGPU_STOP_PERIODIC;
+      return true;
+    }
+    return false;
+  };
+  // Could an accepted step from tb to ta trigger a snapshot or complete a
+  // resampled period (the only time the detector can fire)? Such steps run
+  // as single-step batches, so that their input field is still intact.
+  const double dt_s = d.t_per / cfg->detector_samples_per_period;
+  const long S = cfg->detector_samples_per_period;
+  auto eventful = [&](double tb, double ta) {
+    const long pi = std::max(period_idx, static_cast<long>(std::floor(tb / d.t_per)));
+    for (long q = pi - 1; q <= pi + 1; ++q) {
+      const double e = static_cast<double>(q) * d.t_per;
+      if (cfg->snapshot_pre_on && ta >= e && tb < e) return true;
+    }
+    if (cfg->snapshot_post_off && ta >= static_cast<double>(off_idx) * d.t_per + off_offset)
+      return true;
+    for (size_t q = next_time; q < pending.size(); ++q)
+      if (ta >= pending[q]) return true;
+    if (detect) {  // a sample index k = S-1 (mod S) with tb <= k*dt <= ta
+      // (>= tb: conservative at the seed's sample 0)
+      long k = static_cast<long>(std::floor(tb / dt_s));
+      k = k - ((k % S) + S) % S + (S - 1);
+      while (static_cast<double>(k) * dt_s < tb) k += S;
+      while (k >= S && static_cast<double>(k - S) * dt_s >= tb) k -= S;
+      if (static_cast<double>(k) * dt_s <= ta) return true;
+    }
+    return false;
+  };
+  bool fired = false;
+  while (!fired) {
+    if (t >= cfg->t_end) {
+      stop = PCGPU_STOP_REACHED_TIME;
       break;
     }
+    if (resident) {
+      // schedule: steps from (t, comp) assuming no halving, ending before an
+      // eventful step (or with it alone), or once t_end is reached
+      int n = 0;
+      double tt = t, cc = comp;
+      while (n < pcgpu_stepper::kResBatch && tt < cfg->t_end) {
+        const double tau0 = h->initial_tau(tt);
+        const double y = tau0 - cc;
+        const double ta = tt + y;
+        const bool ev = eventful(tt, ta);
+        if (ev && n > 0) break;
+        h->res_entry(h->res_sched_host[n], tt, tau0);
+        ++n;
+        cc = (ta - tt) - y;
+        tt = ta;
+        if (ev) break;
+      }
+      const int s0 = state;
+      const ResCtl c = h->res_batch(X, state, n, np);
+      for (int q = 0; q < c.steps && !fired; ++q) {
+        const ResLog& lg = h->res_log_host[q];
+        // single-step batches keep the step's input field intact
+        const int sq = c.steps == 1 ? c.state : -1;
+        fired = after_step(lg.r, c.steps == 1 ? X[s0] : nullptr, sq >= 0 ? X[sq] : nullptr,
+                           lg.probes);
+      }
+      state = c.state;
+      if (fired) break;
+      if (c.stop == kResFloor) {  // the field stays the last accepted one
+        h->res_fail(c, t);
+        stop = PCGPU_STOP_TAU_FLOOR;
+        break;
+      }
+      if (c.stop == kResError) {
+        const int rc = h->res_fail(c, t);
+        h->buf[kField] = X[state];
+        h->buf[kNext] = X[(state + 1) % 3];
+        h->buf[kIterT] = X[(state + 2) % 3];
+        return rc;
+      }
+      if (c.stop == kResNeedHost) {
+        const int s1 = state;
+        pcgpu_step_result r;
+        double upd = 0;
+        const int rc = h->res_host_step(X, &state, t, -1.0, &r, &upd);
+        if (rc == PCGPU_ERR_TAU_FLOOR) {
+          stop = PCGPU_STOP_TAU_FLOOR;
+          break;
+        }
+        if (rc) return rc;
+        gather(X[state]);
+        fired = after_step(r, X[s1], X[state], h_vals);
+      }
+      continue;
+    }
+    // host-driven step on the rotation
+    const int s1 = state;
+    pcgpu_step_result r;
+    double upd = 0;
+    const int rc = h->res_host_step(X, &state, t, -1.0, &r, &upd);
+    if (rc == PCGPU_ERR_TAU_FLOOR) {  // the field stays the last accepted one
+      stop = PCGPU_STOP_TAU_FLOOR;
+      break;
+    }
+    if (rc) {
+      h->buf[kField] = X[state];
+      h->buf[kNext] = X[(state + 1) % 3];
+      h->buf[kIterT] = X[(state + 2) % 3];
+      return rc;
+    }
+    gather(X[state]);
+    fired = after_step(r, X[s1], X[state], h_vals);
   }
-  h->buf[kField] = cur;
-  h->buf[kNext] = nxt;
-  h->buf[kIterT] = spare;
-  h->from_state(cur, field);
+  h->buf[kField] = X[state];
+  h->buf[kNext] = X[(state + 1) % 3];
+  h->buf[kIterT] = X[(state + 2) % 3];
+  h->from_state(X[state], field);
   CK(cudaStreamSynchronize(h->stream));
   res->t = t;
   res->reason = stop;
   if (!h->runner) h->runner = new pcgpu_runner_state();
-  h->runner->detector_rows = detect ? det.rs.rows : std::vector<std::vector<double>>{};
+  h->runner->detector_rows =
+      detect && !cfg->detect ? det.rs.rows : std::vector<std::vector<double>>{};
   h->runner->samples = cfg->detector_samples_per_period;
   res->detector_periods = static_cast<int32_t>(h->runner->detector_rows.size());
   GUARD_END(h)
@@ -1591,6 +1936,7 @@ int pcgpu_evolve_host(pcgpu_stepper* h, double* field_host, const pcgpu_runner_c
                       pcgpu_step_cb on_step, pcgpu_snapshot_cb on_snapshot, void* user,
                       pcgpu_evolve_result* res) {
   if (!h || !field_host) return PCGPU_ERR_ARG;
+  DeviceGuard dg(h->d.device);
   // Trampolines: the step callback passes through, snapshots are copied to a
   // host buffer first.
   struct Ctx {

@@ -15,10 +15,10 @@
 //   bit pattern of a non-negative double), so every rank takes the same
 //   convergence / tau-halving decisions without host round trips.
 //
-// The per-cell and per-line arithmetic is exactly the single-GPU fast path's
-// (adi_fast.cu slab kernels), so a partitioned run is bit-identical to a
-// single-GPU fast run: tests run P "virtual ranks" in one process on one GPU
-// (Comm::Local) and compare bit-for-bit. Real ranks (one process per GPU)
+// The per-cell and per-line arithmetic is exactly the single-GPU exact
+// path's (adi_exact.cu slab kernels), so a partitioned run is bit-identical to
+// a single-GPU run (and so to the reference): tests run P "virtual ranks" in
+// one process on one GPU (Comm::Local) and compare bit-for-bit. Real ranks (one process per GPU)
 // use NCCL (grouped ncclSend/ncclRecv for the all-to-all, ncclAllReduce for
 // the norm), loaded with dlopen so the single-GPU library has no NCCL
 // dependency.
@@ -177,7 +177,7 @@ struct RankState {
   int i0 = 0, ni = 0;  // r-slab lines
   double *zTc = nullptr, *zExpl = nullptr, *zHalf = nullptr, *zIter = nullptr, *zR = nullptr;
   double *rHalf = nullptr, *rExpl = nullptr, *rOut = nullptr, *rIter = nullptr;
-  double *send = nullptr, *recv = nullptr;
+  double* recv = nullptr;
   // exact mode: Thomas scratch on both slabs, K-bar and the r-slab copy of
   // the step's anchor (Lambda_z is recomputed from it every attempt, like the
   // single-GPU stepper)
@@ -236,7 +236,6 @@ struct pcgpu_dist {
     return p;
   }
 
-  bool exact() const { return d.mode == PCGPU_MODE_EXACT; }
   int zcount(int p) const { return zb[p + 1] - zb[p]; }
   int rcount(int p) const { return rb[p + 1] - rb[p]; }
 
@@ -277,97 +276,6 @@ struct pcgpu_dist {
                          stream));
     NCK(g_nccl.allReduce(&R.st->err, &R.st->err, 1, ncclUint64, ncclMin, comm, stream));
     NCK(g_nccl.groupEnd());
-  }
-
-  // All-to-all transpose of two fields. z->r: sources are z-slab N-layout
-  // buffers (lines j, stride nr), destinations r-slab T-layout (lines i,
-  // stride nz). r->z the reverse. Packed block (p -> q) for z->r is
-  // [i in R_q][j in Z_p]; for r->z it is [j in Z_q][i in R_p].
-  void transpose(bool z2r, double* const* srcA, double* const* srcB, double* const* dstA,
-                 double* const* dstB) {
-    if (timing) DCK(cudaEventRecord(ev0, stream));
-    const int nr = d.nr, nz = d.nz;
-    // pack (every local rank, every destination)
-    for (size_t lr = 0; lr < ranks.size(); ++lr) {
-      RankState& R = ranks[lr];
-      size_t off = 0;
-      for (int q = 0; q < nranks; ++q) {
-        const int rows = z2r ? R.nj : R.ni;             // source lines owned
-        const int cols = z2r ? rcount(q) : zcount(q);   // destination's lines
-        const int c0 = z2r ? rb[q] : zb[q];
-        const long long ld = z2r ? nr : nz;
-        const size_t blk = static_cast<size_t>(rows) * cols;
-        transpose_block(srcA[lr] + c0, ld, rows, cols, R.send + off, rows, stream);
-        transpose_block(srcB[lr] + c0, ld, rows, cols, R.send + off + blk, rows, stream);
-        off += 2 * blk;
-      }
-    }
-    // exchange
-    if (local) {
-      for (int p = 0; p < nranks; ++p) {
-        size_t soff = 0;
-        for (int q = 0; q < nranks; ++q) {
-          const size_t blk = static_cast<size_t>(z2r ? zcount(p) * rcount(q)
-                                                     : rcount(p) * zcount(q));
-          // receiver q's staging: blocks ordered by source p
-          size_t roff = 0;
-          for (int pp = 0; pp < p; ++pp)
-            roff += 2 * static_cast<size_t>(z2r ? zcount(pp) * rcount(q) : rcount(pp) * zcount(q));
-          DCK(cudaMemcpyAsync(ranks[q].recv + roff, ranks[p].send + soff,
-                              sizeof(double) * 2 * blk, cudaMemcpyDeviceToDevice, stream));
-          soff += 2 * blk;
-        }
-      }
-    } else {
-      RankState& R = ranks[0];
-      const int me = R.rank;
-      NCK(g_nccl.groupStart());
-      size_t soff = 0, roff = 0;
-      for (int q = 0; q < nranks; ++q) {
-        const size_t sblk = static_cast<size_t>(z2r ? zcount(me) * rcount(q)
-                                                    : rcount(me) * zcount(q));
-        const size_t rblk = static_cast<size_t>(z2r ? zcount(q) * rcount(me)
-                                                    : rcount(q) * zcount(me));
-        if (sblk) NCK(g_nccl.send(R.send + soff, 2 * sblk, ncclDouble, q, comm, stream));
-        if (rblk) NCK(g_nccl.recv(R.recv + roff, 2 * rblk, ncclDouble, q, comm, stream));
-        soff += 2 * sblk;
-        roff += 2 * rblk;
-      }
-      NCK(g_nccl.groupEnd());
-    }
-    // unpack (2-D copies into the destination layout)
-    for (size_t lr = 0; lr < ranks.size(); ++lr) {
-      RankState& R = ranks[lr];
-      const int me = R.rank;
-      size_t off = 0;
-      for (int p = 0; p < nranks; ++p) {
-        // block from p: z2r -> [i in R_me][j in Z_p] into T layout lines i, cols j
-        //               r2z -> [j in Z_me][i in R_p] into N layout lines j, cols i
-        const int rows = z2r ? R.ni : R.nj;
-        const int cols = z2r ? zcount(p) : rcount(p);
-        const int c0 = z2r ? zb[p] : rb[p];
-        const size_t ld = z2r ? nz : nr;
-        const size_t blk = static_cast<size_t>(rows) * cols;
-        if (blk) {
-          DCK(cudaMemcpy2DAsync(dstA[lr] + c0, ld * sizeof(double), R.recv + off,
-                                cols * sizeof(double), cols * sizeof(double), rows,
-                                cudaMemcpyDeviceToDevice, stream));
-          DCK(cudaMemcpy2DAsync(dstB[lr] + c0, ld * sizeof(double), R.recv + off + blk,
-                                cols * sizeof(double), cols * sizeof(double), rows,
-                                cudaMemcpyDeviceToDevice, stream));
-        }
-        off += 2 * blk;
-        (void)me;
-      }
-    }
-    ++transposes;
-    if (timing) {
-      DCK(cudaEventRecord(ev1, stream));
-      DCK(cudaEventSynchronize(ev1));
-      float ms = 0;
-      DCK(cudaEventElapsedTime(&ms, ev0, ev1));
-      transpose_ms += ms;
-    }
   }
 
   void reset_status(bool clear_err = true) {
@@ -624,77 +532,7 @@ struct pcgpu_dist {
   // One ADI step (solver.cpp:356-373) on the partitioned state
   // (z-slab anchor zTc + zExpl = Lambda_z[zTc]).
   int step(double t, pcgpu_step_result* r, double* updates) {
-    return exact() ? step_exact(t, r, updates) : step_fast(t, r, updates);
-  }
-
-  int step_fast(double t, pcgpu_step_result* r, double* updates) {
-    double tau = pcgpu_host_initial_tau(d, t);
-    *r = pcgpu_step_result{};
-    for (;;) {
-      const double pulse = d.source_kind == PCGPU_SOURCE_JOULE
-                               ? pcgpu_host_pulse_value(d, t + 0.5 * tau) : 0.0;
-      const double hk = 2.0 / tau;
-      // ---- radial half-step on the z-slabs ----
-      reset_status();
-      auto zsrc = [&](RankState& R, int it) -> const double* {
-        return it == 1 ? R.zTc : (it % 2 == 0 ? R.zHalf : R.zIter);
-      };
-      auto zdst = [&](RankState& R, int it) -> double* { return it % 2 == 1 ? R.zHalf : R.zIter; };
-      int conv = picard(pred_r, [&](size_t lr, int it) {
-        RankState& R = ranks[lr];
-        launch_radial_fast_slab(P, it, d.epsilon, hk, pulse, R.j0, R.nj, zsrc(R, it), R.zTc,
-                                R.zExpl, zdst(R, it), R.st, stream);
-      }, &r->radial, true);
-      if (conv < 0) return -conv;
-      *updates += static_cast<double>(active) * r->radial.iterations;
-      if (conv > 0) {
-        // explicit radial term on the z-slab, then z -> r transpose of (T_half, expl)
-        std::vector<double*> hA(ranks.size()), hB(ranks.size()), dA(ranks.size()), dB(ranks.size());
-        for (size_t lr = 0; lr < ranks.size(); ++lr) {
-          RankState& R = ranks[lr];
-          hA[lr] = zdst(R, conv);
-          launch_rhs_zslab(P, pulse, R.j0, R.nj, hA[lr], R.zR, R.st, stream);
-          hB[lr] = R.zR;
-          dA[lr] = R.rHalf;
-          dB[lr] = R.rExpl;
-        }
-        transpose(true, hA.data(), hB.data(), dA.data(), dB.data());
-        // ---- axial half-step on the r-slabs ----
-        reset_status();
-        auto rsrc = [&](RankState& R, int it) -> const double* {
-          return it == 1 ? R.rHalf : (it % 2 == 0 ? R.rOut : R.rIter);
-        };
-        auto rdst = [&](RankState& R, int it) -> double* { return it % 2 == 1 ? R.rOut : R.rIter; };
-        const int aconv = picard(pred_a, [&](size_t lr, int it) {
-          RankState& R = ranks[lr];
-          launch_axial_fast_slab(P, it, d.epsilon, hk, R.i0, R.ni, rsrc(R, it), R.rHalf,
-                                 R.rExpl, rdst(R, it), R.st, stream);
-        }, &r->axial, false);
-        if (aconv < 0) return -aconv;
-        *updates += static_cast<double>(active) * r->axial.iterations;
-        if (aconv > 0) {
-          // accept: Lambda_z[T_new] on the r-slab, r -> z transpose of (T_new, expl)
-          for (size_t lr = 0; lr < ranks.size(); ++lr) {
-            RankState& R = ranks[lr];
-            hA[lr] = rdst(R, aconv);
-            launch_expl_rslab(P, R.i0, R.ni, hA[lr], R.rHalf, R.st, stream);
-            hB[lr] = R.rHalf;
-            dA[lr] = R.zTc;
-            dB[lr] = R.zExpl;
-          }
-          transpose(false, hA.data(), hB.data(), dA.data(), dB.data());
-          r->tau_used = tau;
-          return PCGPU_OK;
-        }
-      }
-      tau *= 0.5;
-      ++r->halvings;
-      if (tau < tau_floor) {
-        err = "time step fell below floor";
-        return PCGPU_ERR_TAU_FLOOR;
-      }
-      r->axial = pcgpu_outcome{};
-    }
+    return step_exact(t, r, updates);
   }
 };
 
@@ -716,18 +554,22 @@ int pcgpu_dist_create(const pcgpu_desc* d, int32_t rank, int32_t nranks, const v
   if (!d || !out || nranks < 1) return PCGPU_ERR_ARG;
   *out = nullptr;
   std::string v = pcgpu_validate_desc(d);
-  if (v.empty() && d->mode == PCGPU_MODE_EXACT && d->source_kind == PCGPU_SOURCE_FIELD)
-    v = "pcgpu_dist: exact mode supports Null and Joule sources";
+  if (v.empty() && d->source_kind == PCGPU_SOURCE_FIELD)
+    v = "pcgpu_dist: the partitioned stepper supports Null and Joule sources";
   if (!v.empty()) {
     g_dist_create_error = v;
     return PCGPU_ERR_CONFIG;
+  }
+  DeviceGuard dg(d->device);
+  if (!dg.ok) {
+    g_dist_create_error = "pcgpu_dist_create: cannot select device";
+    return PCGPU_ERR_CUDA;
   }
   auto h = std::make_unique<pcgpu_dist>();
   try {
     h->d = *d;
     h->nranks = nranks;
     h->local = nccl_id == nullptr;
-    DCK(cudaSetDevice(d->device));
     DCK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     DCK(cudaEventCreate(&h->ev0));
     DCK(cudaEventCreate(&h->ev1));
@@ -770,18 +612,13 @@ int pcgpu_dist_create(const pcgpu_desc* d, int32_t rank, int32_t nranks, const v
       R.rOut = h->alloc(rc);
       R.rIter = h->alloc(rc);
       // staging: z->r sends 2*zc, receives 2*rc; r->z the reverse
-      if (d->mode == PCGPU_MODE_EXACT) {
-        R.zW = h->alloc(zc);
-        R.zX = h->alloc(zc);
-        R.rW = h->alloc(rc);
-        R.rX = h->alloc(rc);
-        R.rKbar = h->alloc(rc);
-        R.rTc = h->alloc(rc);
-        R.recv = h->alloc(2 * std::max(zc, rc));  // sends go straight from the fields
-      } else {
-        R.send = h->alloc(2 * std::max(zc, rc));
-        R.recv = h->alloc(2 * std::max(zc, rc));
-      }
+      R.zW = h->alloc(zc);
+      R.zX = h->alloc(zc);
+      R.rW = h->alloc(rc);
+      R.rX = h->alloc(rc);
+      R.rKbar = h->alloc(rc);
+      R.rTc = h->alloc(rc);
+      R.recv = h->alloc(2 * std::max(zc, rc));  // sends go straight from the fields
       DevStatus* st = nullptr;
       DCK(cudaMalloc(&st, sizeof(DevStatus)));
       h->allocs.push_back(st);
@@ -813,7 +650,11 @@ int pcgpu_dist_create(const pcgpu_desc* d, int32_t rank, int32_t nranks, const v
   return PCGPU_OK;
 }
 
-void pcgpu_dist_destroy(pcgpu_dist* h) { delete h; }
+void pcgpu_dist_destroy(pcgpu_dist* h) {
+  if (!h) return;
+  DeviceGuard dg_(h->d.device);
+  delete h;
+}
 
 const char* pcgpu_dist_last_error(const pcgpu_dist* h) {
   return h ? h->err.c_str() : g_dist_create_error.c_str();
@@ -832,44 +673,21 @@ int pcgpu_dist_slabs(const pcgpu_dist* h, int32_t* z0, int32_t* z1, int32_t* r0,
 // Every rank passes the full initial field (device, N layout). Each rank
 // keeps its z-slab lines and Lambda_z on them (computed on the full field).
 int pcgpu_dist_set_field(pcgpu_dist* h, const double* fieldN) {
-  if (h->exact()) {
-    try {
-      const int nr = h->d.nr;
-      for (RankState& R : h->ranks) {
-        // z-slab T layout [i][j - j0] <- N rows j0 .. j0+nj-1
-        transpose_block(fieldN + static_cast<size_t>(R.j0) * nr, nr, R.nj, nr, R.zTc, R.nj,
-                        h->stream);
-        // r-slab N layout [j][i - i0] <- columns i0 .. i0+ni-1
-        if (R.ni)
-          DCK(cudaMemcpy2DAsync(R.rTc, sizeof(double) * R.ni, fieldN + R.i0,
-                                sizeof(double) * nr, sizeof(double) * R.ni, h->d.nz,
-                                cudaMemcpyDeviceToDevice, h->stream));
-      }
-      DCK(cudaStreamSynchronize(h->stream));
-    } catch (const DistError& e) {
-      h->err = e.what;
-      return e.code;
-    }
-    return PCGPU_OK;
-  }
+  if (!h) return PCGPU_ERR_ARG;
+  DeviceGuard dg_(h->d.device);
   try {
-    const int nr = h->d.nr, nz = h->d.nz;
-    const size_t cells = static_cast<size_t>(nr) * nz;
-    double *fT = nullptr, *eT = nullptr;
-    DCK(cudaMalloc(&fT, sizeof(double) * cells));
-    DCK(cudaMalloc(&eT, sizeof(double) * cells));
-    transpose_block(fieldN, nr, nz, nr, fT, nz, h->stream);  // N [j][i] -> T [i][j]
-    launch_expl_rslab(h->P, 0, nr, fT, eT, h->ranks[0].st, h->stream);
+    const int nr = h->d.nr;
     for (RankState& R : h->ranks) {
-      DCK(cudaMemcpyAsync(R.zTc, fieldN + static_cast<size_t>(R.j0) * nr,
-                          sizeof(double) * static_cast<size_t>(R.nj) * nr,
-                          cudaMemcpyDeviceToDevice, h->stream));
-      // Lambda_z of lines Z_r: T-layout columns j0..j0+nj of eT -> N rows
-      transpose_block(eT + R.j0, nz, nr, R.nj, R.zExpl, nr, h->stream);
+      // z-slab T layout [i][j - j0] <- N rows j0 .. j0+nj-1
+      transpose_block(fieldN + static_cast<size_t>(R.j0) * nr, nr, R.nj, nr, R.zTc, R.nj,
+                      h->stream);
+      // r-slab N layout [j][i - i0] <- columns i0 .. i0+ni-1
+      if (R.ni)
+        DCK(cudaMemcpy2DAsync(R.rTc, sizeof(double) * R.ni, fieldN + R.i0, sizeof(double) * nr,
+                              sizeof(double) * R.ni, h->d.nz, cudaMemcpyDeviceToDevice,
+                              h->stream));
     }
     DCK(cudaStreamSynchronize(h->stream));
-    cudaFree(fT);
-    cudaFree(eT);
   } catch (const DistError& e) {
     h->err = e.what;
     return e.code;
@@ -879,19 +697,15 @@ int pcgpu_dist_set_field(pcgpu_dist* h, const double* fieldN) {
 
 // Writes each local rank's z-slab lines into the full-size N-layout buffer.
 int pcgpu_dist_get_field(pcgpu_dist* h, double* fieldN) {
+  if (!h) return PCGPU_ERR_ARG;
+  DeviceGuard dg_(h->d.device);
   try {
     const int nr = h->d.nr;
-    for (RankState& R : h->ranks) {
-      if (h->exact()) {  // r-slab N layout [j][i - i0] -> columns i0 .. i0+ni-1
-        if (R.ni)
-          DCK(cudaMemcpy2DAsync(fieldN + R.i0, sizeof(double) * nr, R.rTc,
-                                sizeof(double) * R.ni, sizeof(double) * R.ni, h->d.nz,
-                                cudaMemcpyDeviceToDevice, h->stream));
-      } else
-        DCK(cudaMemcpyAsync(fieldN + static_cast<size_t>(R.j0) * nr, R.zTc,
-                            sizeof(double) * static_cast<size_t>(R.nj) * nr,
-                            cudaMemcpyDeviceToDevice, h->stream));
-    }
+    for (RankState& R : h->ranks)  // r-slab N layout [j][i - i0] -> columns i0 .. i0+ni-1
+      if (R.ni)
+        DCK(cudaMemcpy2DAsync(fieldN + R.i0, sizeof(double) * nr, R.rTc, sizeof(double) * R.ni,
+                              sizeof(double) * R.ni, h->d.nz, cudaMemcpyDeviceToDevice,
+                              h->stream));
     DCK(cudaStreamSynchronize(h->stream));
   } catch (const DistError& e) {
     h->err = e.what;
@@ -901,10 +715,8 @@ int pcgpu_dist_get_field(pcgpu_dist* h, double* fieldN) {
 }
 
 int pcgpu_dist_set_field_host(pcgpu_dist* h, const double* host) {
-  if (!h->exact()) {
-    h->err = "pcgpu_dist_set_field_host: exact mode only";
-    return PCGPU_ERR_CONFIG;
-  }
+  if (!h) return PCGPU_ERR_ARG;
+  DeviceGuard dg_(h->d.device);
   try {
     const int nr = h->d.nr;
     std::vector<double*> a, b;
@@ -933,10 +745,8 @@ int pcgpu_dist_set_field_host(pcgpu_dist* h, const double* host) {
 }
 
 int pcgpu_dist_get_field_host(pcgpu_dist* h, double* host) {
-  if (!h->exact()) {
-    h->err = "pcgpu_dist_get_field_host: exact mode only";
-    return PCGPU_ERR_CONFIG;
-  }
+  if (!h) return PCGPU_ERR_ARG;
+  DeviceGuard dg_(h->d.device);
   try {
     const int nr = h->d.nr;
     for (RankState& R : h->ranks)
@@ -954,6 +764,8 @@ int pcgpu_dist_get_field_host(pcgpu_dist* h, double* host) {
 
 int pcgpu_dist_run(pcgpu_dist* h, double t0, int32_t nsteps, pcgpu_step_result* results,
                    pcgpu_run_stats* stats) {
+  if (!h) return PCGPU_ERR_ARG;
+  DeviceGuard dg_(h->d.device);
   pcgpu_run_stats s{};
   double t = t0;
   int rc = PCGPU_OK;
@@ -987,7 +799,9 @@ int pcgpu_dist_run(pcgpu_dist* h, double t0, int32_t nsteps, pcgpu_step_result* 
 int32_t pcgpu_dist_transport(const pcgpu_dist* h) { return h->peer ? 1 : 0; }
 
 int pcgpu_dist_ipc_export(pcgpu_dist* h, void* handles) {
-  if (!h || !handles || !h->exact() || h->local) return PCGPU_ERR_ARG;
+  if (!h) return PCGPU_ERR_ARG;
+  DeviceGuard dg_(h->d.device);
+  if (!h || !handles || h->local) return PCGPU_ERR_ARG;
   try {
     RankState& R = h->ranks[0];
     double* bufs[4] = {R.zTc, R.zExpl, R.rHalf, R.rExpl};
@@ -1005,7 +819,9 @@ int pcgpu_dist_ipc_export(pcgpu_dist* h, void* handles) {
 }
 
 int pcgpu_dist_ipc_import(pcgpu_dist* h, const void* all_handles) {
-  if (!h || !all_handles || !h->exact() || h->local) return PCGPU_ERR_ARG;
+  if (!h) return PCGPU_ERR_ARG;
+  DeviceGuard dg_(h->d.device);
+  if (!h || !all_handles || h->local) return PCGPU_ERR_ARG;
   try {
     const auto* in = static_cast<const unsigned char*>(all_handles);
     PeerSlabs ps{};
@@ -1051,8 +867,9 @@ int pcgpu_dist_ipc_import(pcgpu_dist* h, const void* all_handles) {
 
 int pcgpu_dist_peer_off(pcgpu_dist* h) {
   if (!h) return PCGPU_ERR_ARG;
+  DeviceGuard dg_(h->d.device);
+  if (!h) return PCGPU_ERR_ARG;
   if (h->local) return PCGPU_OK;  // emulated ranks: peer stores into local slabs
-  if (cudaSetDevice(h->d.device) != cudaSuccess) return PCGPU_ERR_CUDA;
   cudaStreamSynchronize(h->stream);
   for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
   h->ipc_opened.clear();

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "../../include/pcgpu.h"
+#include "adi_kernels.h"
 #include "extents.h"
 
 namespace {
@@ -187,8 +188,8 @@ int pcgpu_writer_create(const pcgpu_desc* d, const double* z_center, int32_t slo
   w->r_center.assign(d->r_center, d->r_center + d->nr);
   w->z_center.assign(z_center, z_center + d->nz);
   w->layer.assign(d->layer, d->layer + d->nr);
-  bool ok = cudaSetDevice(d->device) == cudaSuccess &&
-            cudaStreamCreateWithFlags(&w->copy_stream, cudaStreamNonBlocking) == cudaSuccess;
+  pcgpu::DeviceGuard dg(d->device);
+  bool ok = dg.ok && cudaStreamCreateWithFlags(&w->copy_stream, cudaStreamNonBlocking) == cudaSuccess;
   w->slots.resize(slots);
   for (Slot& s : w->slots) {
     ok = ok && cudaMalloc(&s.dev, sizeof(double) * w->cells()) == cudaSuccess &&
@@ -204,7 +205,11 @@ int pcgpu_writer_create(const pcgpu_desc* d, const double* z_center, int32_t slo
   return PCGPU_OK;
 }
 
-void pcgpu_writer_destroy(pcgpu_writer* w) { delete w; }
+void pcgpu_writer_destroy(pcgpu_writer* w) {
+  if (!w) return;
+  pcgpu::DeviceGuard dg(w->device);
+  delete w;
+}
 
 int pcgpu_writer_submit(pcgpu_writer* w, const double* field_dev, void* stream,
                         const char* path, int32_t format, const char* header) {
@@ -225,6 +230,7 @@ int pcgpu_writer_submit(pcgpu_writer* w, const double* field_dev, void* stream,
     w->slots[slot].busy = true;
   }
   Slot& s = w->slots[slot];
+  pcgpu::DeviceGuard dg(w->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaEvent_t ready = nullptr;
   bool ok = cudaMemcpyAsync(s.dev, field_dev, sizeof(double) * w->cells(),

@@ -7,8 +7,7 @@ runs the z-slab radial sweep, the all-to-all transposes and the per-iteration
 allreduce(max) of the Picard norm itself (NCCL on the library's stream).
 With ``emulate=P`` the library runs P virtual ranks in this process on one
 GPU -- the same code path minus NCCL -- which is how the partitioned path is
-validated on a single GPU (bit-identical to the single-GPU stepper of the
-same mode).
+validated on a single GPU (bit-identical to the single-GPU stepper).
 """
 from __future__ import annotations
 
@@ -27,7 +26,7 @@ def slab_plan(grid, mats, source, timing, cfg, nranks: int) -> Tuple[List[int], 
     """Slab boundaries (host only, no GPU): rank p owns radial lines
     [zb[p], zb[p+1]) and axial lines [rb[p], rb[p+1])."""
     lib = N.load()
-    desc, keep = build_desc(grid, mats, source, timing, cfg, N.MODE_FAST, 0)
+    desc, keep = build_desc(grid, mats, source, timing, cfg, N.MODE_EXACT, 0)
     zb = (C.c_int32 * (nranks + 1))()
     rb = (C.c_int32 * (nranks + 1))()
     rc = lib.pcgpu_dist_plan(C.byref(desc), nranks, zb, rb)
@@ -72,9 +71,8 @@ def allgather_bytes(mine: bytes) -> bytes:
 class PartitionedAdi:
     """z-slab / r-slab partitioned AdiStepper.
 
-    mode "exact": the exact kernels on dense slabs -- bit-identical to the
-    single-GPU exact stepper (and so to the reference); mode "fast": the
-    partitioned fast-mode line solver."""
+    The exact kernels on dense slabs -- bit-identical to the single-GPU
+    stepper (and so to the reference)."""
 
     def __init__(self, grid, mats, source, timing, cfg, device: int = 0,
                  rank: int = 0, world: int = 1, emulate: Optional[int] = None,
@@ -84,11 +82,10 @@ class PartitionedAdi:
         timing.validate()
         self._grid = grid
         self._nr, self._nz = grid.nr(), grid.nz()
-        if mode not in ("exact", "fast"):
-            raise ValueError("mode must be 'exact' or 'fast'")
+        if mode != "exact":
+            raise ConfigError(f"exec.mode: unknown mode {mode!r} (only 'exact' exists)")
         self.mode = mode
-        self._desc, self._keep = build_desc(grid, mats, source, timing, cfg,
-                                            N.MODE_EXACT if mode == "exact" else N.MODE_FAST,
+        self._desc, self._keep = build_desc(grid, mats, source, timing, cfg, N.MODE_EXACT,
                                             device)
         h = C.c_void_p()
         if emulate is not None:

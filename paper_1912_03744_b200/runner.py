@@ -125,7 +125,9 @@ class RunnerCfgC(C.Structure):
                 ("n_snapshot_times", C.c_int32), ("snapshot_times", C.POINTER(C.c_double)),
                 ("snapshot_pre_on", C.c_int32), ("snapshot_post_off", C.c_int32),
                 ("detector_samples_per_period", C.c_int32), ("detector_min_periods", C.c_int32),
-                ("detector_tolerance", C.c_double), ("source_on", C.c_int32)]
+                ("detector_tolerance", C.c_double), ("source_on", C.c_int32),
+                # NULL: the library's restatement of RegimeDetector (runner.cpp:35-95)
+                ("detect", C.c_void_p), ("detect_user", C.c_void_p)]
 
 
 class EvolveResultC(C.Structure):

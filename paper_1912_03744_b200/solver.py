@@ -3,7 +3,7 @@
 Same constructor arguments, method names, argument meaning and error
 behaviour as the reference; the work happens in libpcgpu.so (hand-written
 sm_100a FP64 kernels) through the C-ABI of include/pcgpu.h. The reference's
-LinePool argument becomes a DevicePlan (which GPU, exact or fast mode).
+LinePool argument becomes a DevicePlan (which GPU).
 
 Fields are float64 (nr, nz) arrays in the reference's column-major Array2
 layout: numpy arrays with order='F' (host; copied through the *_host entry
@@ -102,14 +102,15 @@ class StepResult:  # solver.hpp:56-60
 
 @dataclass
 class DevicePlan:
-    """Replaces the reference's ExecPlan/LinePool: which GPU, which kernels."""
+    """Replaces the reference's ExecPlan/LinePool: which GPU. The kernels are
+    bit-identical to the reference ("exact", the only mode)."""
     device: int = 0
-    mode: str = "exact"  # "exact" (bit-identical to the reference) or "fast"
+    mode: str = "exact"
 
     def mode_id(self) -> int:
-        if self.mode not in ("exact", "fast"):
-            raise ConfigError(f"exec.mode: unknown mode {self.mode!r}")
-        return N.MODE_EXACT if self.mode == "exact" else N.MODE_FAST
+        if self.mode != "exact":
+            raise ConfigError(f"exec.mode: unknown mode {self.mode!r} (only 'exact' exists)")
+        return N.MODE_EXACT
 
 
 def _outcome(o: N.Outcome) -> HalfStepOutcome:
@@ -173,7 +174,9 @@ class AdiStepper:
         msg = self._lib.pcgpu_last_error(self._h).decode()
         line = int(self._lib.pcgpu_error_line(self._h))
         if rc == N.ERR_TAU_FLOOR:
-            raise TauFloorError(msg)
+            tau, floor, t = C.c_double(), C.c_double(), C.c_double()
+            self._lib.pcgpu_last_tau_floor(self._h, C.byref(tau), C.byref(floor), C.byref(t))
+            raise TauFloorError(msg, tau.value, floor.value, t.value)
         if rc == N.ERR_TABLE_RANGE:
             raise LineError(line, msg, TableRangeError)
         if rc == N.ERR_ZERO_PIVOT:
@@ -318,6 +321,16 @@ class AdiStepper:
 
     def launch_count(self) -> int:
         return int(self._lib.pcgpu_launch_count(self._h))
+
+    def resident_stats(self) -> dict:
+        """The resident stepper (whole steps in one cooperative launch per
+        batch; pcgpu_resident_stats): grid size (0: not used on this grid),
+        batches, steps, steps redone host-driven."""
+        g = C.c_int32()
+        b, s, hs = C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(self._lib.pcgpu_resident_stats(self._h, C.byref(g), C.byref(b), C.byref(s),
+                                                   C.byref(hs)))
+        return {"grid": g.value, "batches": b.value, "steps": s.value, "host_steps": hs.value}
 
     def evolve(self, timing, initial, t_end: float, cfg, writer=None, snapshot_file=None):
         """pulsecell::evolve (runner.cpp:97-190) with the field resident on the

@@ -74,7 +74,7 @@ int main() {
   plan.workers = 4;
   LinePool pool(plan);
   pulsecell::AdiStepper cpu(grid, layers, src, timing, cfg, pool);
-  pulsecell::gpu::AdiStepper gpu(grid, layers, src, timing, cfg, {0, true});
+  pulsecell::gpu::AdiStepper gpu(grid, layers, src, timing, cfg, {0});
   Array2 fc = make_field(grid, cfg.T0), fg = make_field(grid, cfg.T0);
   Real t = 0;
   int bad = 0;
@@ -95,14 +95,30 @@ int main() {
   SolverConfig c1 = cfg;
   c1.max_iter = 1;
   c1.tau_min = 0.9 * initial_tau(0.5, timing, cfg);
-  pulsecell::gpu::AdiStepper g1(grid, layers, src, timing, c1, {0, true});
+  pulsecell::gpu::AdiStepper g1(grid, layers, src, timing, c1, {0});
   bool threw = false;
   Array2 f1 = fg;
+  double g_tau = -1, g_floor = -1, g_time = -1, c_tau = -2, c_floor = -2, c_time = -2;
   try {
     g1.step(f1, 0.5);
-  } catch (const TauFloorError&) {
+  } catch (const TauFloorError& e) {
     threw = true;
+    g_tau = e.tau();
+    g_floor = e.floor();
+    g_time = e.time();
   }
+  {  // the reference's own exception carries the same tau / floor / time
+    pulsecell::AdiStepper c1cpu(grid, layers, src, timing, c1, pool);
+    Array2 f1c = fc;
+    try {
+      c1cpu.step(f1c, 0.5);
+    } catch (const TauFloorError& e) {
+      c_tau = e.tau();
+      c_floor = e.floor();
+      c_time = e.time();
+    }
+  }
+  threw = threw && g_tau == c_tau && g_floor == c_floor && g_time == c_time;
   // evolve: the reference's runner on the CPU stepper vs pulsecell::gpu::evolve
   RunnerConfig rc;
   rc.t_end = 0.05;
@@ -113,7 +129,7 @@ int main() {
   c2.tau_transient_divisor = 100;
   c2.tau_source_divisor = 100;
   pulsecell::AdiStepper cpu2(grid, layers, src, timing, c2, pool);
-  pulsecell::gpu::AdiStepper gpu2(grid, layers, src, timing, c2, {0, true});
+  pulsecell::gpu::AdiStepper gpu2(grid, layers, src, timing, c2, {0});
   const EvolutionResult ec = evolve(cpu2, timing, make_field(grid, cfg.T0), rc.t_end, rc);
   const EvolutionResult eg = pulsecell::gpu::evolve(gpu2, timing, make_field(grid, cfg.T0),
                                                     rc.t_end, rc);
@@ -160,7 +176,7 @@ int main() {
   for (size_t k = 0; k < ec.at_times.size(); ++k)
     outputs(ec.at_times[k].field, dc + "/snapshot_t" + std::to_string(k));
   outputs(ec.field, dc + "/field_final");
-  pulsecell::gpu::simulate(grid, layers, src, timing, c2, rc, rc.t_end, dg, header, {0, true});
+  pulsecell::gpu::simulate(grid, layers, src, timing, c2, rc, rc.t_end, dg, header, {0});
   int files = 0, fbad = 0;
   for (const auto& e : fs::directory_iterator(dc)) {
     ++files;
@@ -171,7 +187,7 @@ int main() {
     if (!fs::exists(fs::path(dc) / e.path().filename())) ++fbad;
   fs::remove_all(base);
   // bench --device: the timing loop of bench.cpp on the GPU stepper
-  const BenchReport br = pulsecell::gpu::run_benchmark(grid, layers, src, timing, cfg, 3, {0, true});
+  const BenchReport br = pulsecell::gpu::run_benchmark(grid, layers, src, timing, cfg, 3, {0});
   const bool bench_ok = br.rows.size() == 1 && br.rows[0].wall_s > 0 && br.nr == grid.nr();
   std::printf("dropin: steps with mismatching results %d, masked cells differing %ld, "
               "TauFloorError mapped %s, evolve (%ld steps, %zu snapshots) %s, "
