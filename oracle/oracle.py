@@ -130,6 +130,8 @@ def _load_ref():
             ("pcref_axial_half_step", C.c_int, [_vp, _vp, C.c_double, C.c_double, _vp, O]),
             ("pcref_step", C.c_int, [_vp, _vp, C.c_double, S]),
             ("pcref_run", C.c_int, [_vp, _vp, C.c_double, C.c_int32, S, R]),
+            ("pcref_run_growth", C.c_int, [_vp, _vp, C.c_double, C.c_double, C.c_int32,
+                                           C.c_double, C.c_double, C.c_int32, C.c_double, S, R]),
             ("pcref_evolve", C.c_int, [_vp, _vp, C.POINTER(RefEvolveIO)]),
             ("pcref_write_snapshot", C.c_int, [_vp, _vp, C.c_char_p, C.c_int32, C.c_char_p]),
             ("pcref_write_trace", C.c_int, [_vp, _vp, _vp, C.c_int64, C.c_int32, C.c_char_p,
@@ -196,6 +198,20 @@ class _Base:
         stats = {k: getattr(st, k) for k, _ in N.RunStats._fields_}
         self._check(rc)
         return float(st.t_end), stats, [_result(res[k]) for k in range(nsteps)]
+
+    def run_growth(self, field, t0, t_end, max_steps, policy=None):
+        """The BASELINE growth policy (pcgpu_run_growth's controller): the
+        port's oracle_run_growth, or for RefStepper the reference's own
+        half-steps under the same controller (pcref_run_growth)."""
+        from paper_1912_03744_b200.solver import GrowthPolicy
+        pol = policy or GrowthPolicy()
+        res = (N.StepResultC * max(1, max_steps))()
+        st = N.RunStats()
+        rc = self._call("run_growth", _ptr(field), t0, t_end, int(max_steps), pol.tau_start,
+                        pol.grow, int(pol.easy_steps), pol.tau_max, res, C.byref(st))
+        stats = {k: getattr(st, k) for k, _ in N.RunStats._fields_}
+        self._check(rc)
+        return float(st.t_end), stats, [_result(res[k]) for k in range(int(st.steps))]
 
     def clamp_events(self) -> List[int]:
         arr = (C.c_uint64 * self.n_layers)()
@@ -269,18 +285,6 @@ class OracleError(RuntimeError):
 class PortStepper(_Base):
     """The C restatement, driven by the same descriptor as the GPU library."""
     prefix = "oracle_"
-
-    def run_growth(self, field, t0, t_end, max_steps, policy=None):
-        from paper_1912_03744_b200.solver import GrowthPolicy
-        pol = policy or GrowthPolicy()
-        res = (N.StepResultC * max(1, max_steps))()
-        st = N.RunStats()
-        rc = self.lib.oracle_run_growth(self.h, _ptr(field), t0, t_end, int(max_steps),
-                                        pol.tau_start, pol.grow, int(pol.easy_steps),
-                                        pol.tau_max, res, C.byref(st))
-        stats = {k: getattr(st, k) for k, _ in N.RunStats._fields_}
-        self._check(rc)
-        return float(st.t_end), stats, [_result(res[k]) for k in range(int(st.steps))]
 
     def __init__(self, case, source_kind=None, explicit_extents=False):
         from paper_1912_03744_b200.source import FieldSource, JouleSource, NullSource

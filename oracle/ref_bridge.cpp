@@ -459,4 +459,69 @@ int pcref_thomas_batch(const double* lower, const double* diag, const double* up
   return PCGPU_OK;
 }
 
+// The BASELINE growth policy (pcgpu_run_growth) driven through the
+// reference's own public half-step API (solver.hpp:70-78), the way the
+// reference's acceptance suite drives half-steps (acceptance_main.cpp:311-332,
+// MmsRun::march): each step tries radial then axial at the controller's tau,
+// halves on non-convergence and throws TauFloorError below the floor like
+// AdiStepper::step (solver.cpp:356-373); accepted steps swap the field. The
+// controller itself (grow x`grow` after `easy_steps` steps without halving,
+// cap tau_max) is the policy shared with the GPU and the C restatement.
+int pcref_run_growth(pcref* h, double* field, double t0, double t_end, int32_t max_steps,
+                     double tau_start, double grow, int32_t easy_steps, double tau_max,
+                     pcgpu_step_result* results, pcgpu_run_stats* stats) {
+  pcgpu_run_stats st{};
+  const Grid& g = *h->grid;
+  const double cells = static_cast<double>(g.active_cells());
+  const double floor = h->cfg.effective_tau_min(h->timing.t_per);
+  double t = t0, tau_next = tau_start < tau_max ? tau_start : tau_max;
+  int easy = 0;
+  int rc = PCGPU_OK;
+  try {
+    Array2 f = to_array(h, field);
+    Array2 half = make_field(g, h->cfg.T0), next = make_field(g, h->cfg.T0);
+    for (int32_t k = 0; k < max_steps && t < t_end; ++k) {
+      pcgpu_step_result r{};
+      double tau = tau_next;
+      for (;;) {
+        const HalfStepOutcome rad = h->stepper->radial_half_step(f, t, tau, half);
+        st.cell_updates += cells * rad.iterations;
+        r.radial = pcgpu_outcome{rad.converged ? 1 : 0, rad.iterations, rad.last_delta};
+        r.axial = pcgpu_outcome{};
+        if (rad.converged) {
+          const HalfStepOutcome ax = h->stepper->axial_half_step(half, t, tau, next);
+          st.cell_updates += cells * ax.iterations;
+          r.axial = pcgpu_outcome{ax.converged ? 1 : 0, ax.iterations, ax.last_delta};
+          if (ax.converged) break;
+        }
+        tau *= 0.5;
+        ++r.halvings;
+        if (tau < floor) throw TauFloorError(tau, floor, t);
+      }
+      f.swap(next);
+      r.tau_used = tau;
+      t += tau;
+      if (results) results[k] = r;
+      st.steps += 1;
+      st.halvings += r.halvings;
+      st.radial_iterations += r.radial.iterations;
+      st.axial_iterations += r.axial.iterations;
+      st.cell_updates_accepted += cells * (r.radial.iterations + r.axial.iterations);
+      st.attempt_cells += 2.0 * cells * (r.halvings + 1);
+      easy = r.halvings == 0 ? easy + 1 : 0;
+      tau_next = tau;
+      if (easy >= easy_steps) {
+        tau_next = tau * grow < tau_max ? tau * grow : tau_max;
+        easy = 0;
+      }
+    }
+    std::memcpy(field, f.data(), sizeof(double) * f.size());
+  } catch (const std::exception& e) {
+    rc = h->fail(e);
+  }
+  st.t_end = t;
+  if (stats) *stats = st;
+  return rc;
+}
+
 }  // extern "C"

@@ -67,6 +67,11 @@ int pcref_step(pcref* h, double* field, double t, pcgpu_step_result* result);
 int pcref_run(pcref* h, double* field, double t0, int32_t nsteps, pcgpu_step_result* results,
               pcgpu_run_stats* stats);
 int pcref_clamp_events(const pcref* h, uint64_t* counts);
+/* The BASELINE growth policy over the reference's own radial_half_step /
+ * axial_half_step (same controller as pcgpu_run_growth / oracle_run_growth). */
+int pcref_run_growth(pcref* h, double* field, double t0, double t_end, int32_t max_steps,
+                     double tau_start, double grow, int32_t easy_steps, double tau_max,
+                     pcgpu_step_result* results, pcgpu_run_stats* stats);
 
 /* pulsecell::evolve (runner.cpp:97-190) on the reference stepper, with
  * probes at (r, z). field: initial in, final out. Trace arrays hold

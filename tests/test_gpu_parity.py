@@ -599,6 +599,32 @@ def test_growth_controller_matches_oracle(cuda, name, stepper_path):
     assert np.array_equal(to_host(fg)[g.mask()], fo[g.mask()])
 
 
+def test_growth_controller_cfg2_full_size_vs_reference(cuda):
+    """configs[2] at its full BASELINE size (1024 x 2048) for 200 growth-
+    controller steps: the B200 against the reference's OWN half-steps under
+    the same controller (pcref_run_growth, all host cores) -- identical
+    accepted-dt / halving / Picard-iteration / last_delta sequences and a
+    bit-identical field (north star: identical sequences, <= 1e-6)."""
+    from oracle.oracle import RefStepper, ref_available
+    from paper_1912_03744_b200.solver import GrowthPolicy
+    if not ref_available():
+        pytest.skip("the reference library (oracle/_ref) is not built")
+    case = configs.cfg2()
+    g = case.grid()
+    steps = 200
+    ref = RefStepper(case, workers=os.cpu_count() or 1)
+    fo = make_field(g, case.solver.T0)
+    t_o, _, res_o = ref.run_growth(fo, 0.0, case.t_end, steps, GrowthPolicy())
+    del ref
+    gpu = gpu_stepper(case, "exact")
+    fg = to_dev(make_field(g, case.solver.T0))
+    t_g, _, res_g = gpu.run_growth(fg, 0.0, case.t_end, steps, GrowthPolicy(), keep_results=True)
+    assert len(res_o) == len(res_g) == steps and t_g == t_o
+    assert np.array_equal(_seq(res_g), _seq(res_o))
+    assert max(r.tau_used for r in res_o) > 1e-5  # the controller grew tau
+    assert np.array_equal(to_host(fg)[g.mask()], fo[g.mask()])
+
+
 @pytest.mark.parametrize("name,steps", [("cfg2", 8), ("cfg4", 4)])
 def test_growth_controller_full_size_exact(cuda, name, steps):
     """configs[2] (1024 x 2048) and configs[4] (2048 x 4096 stepped cell) at their
