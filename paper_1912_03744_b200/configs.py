@@ -174,6 +174,62 @@ def paper_like_small(source: int = SOURCE_JOULE) -> Case:
                 SolverConfig(epsilon=1e-8, max_iter=10), source_kind=source)
 
 
+# ---- the reference's own input configuration --------------------------------
+def synthetic_materials(names=("copper_like", "insulator_like", "graphite_like",
+                               "coating_like")) -> List[MaterialTable]:
+    """proj/configs/materials_synthetic.json: the reference's synthetic
+    two-knot tables (the paper's cryogenic data is not available)."""
+    def t(a, b):
+        return PropertyTable([2.0, 400.0], [a, b])
+    table = {
+        "copper_like": MaterialTable("copper_like", 10.0, t(1.8, 2.2), t(800.0, 800.0)),
+        "insulator_like": MaterialTable("insulator_like", 1.0, t(0.05, 0.08), t(0.0008, 0.0012)),
+        "graphite_like": MaterialTable("graphite_like", 1.0, t(0.95, 1.1), t(0.05, 0.09),
+                                       t(100.0, 110.0)),
+        "coating_like": MaterialTable("coating_like", 1.0, t(0.5, 0.6), t(0.5, 0.55)),
+    }
+    return [table[n] for n in names]
+
+
+def paper_cell(steps: int = 2000) -> Case:
+    """proj/configs/paper_cell.json:1-38 -- the paper's 1210 x 100 cell (the grid
+    of PAPER.md's only performance figure): layer radii 0.24/0.245/0.25/0.2501,
+    core 5.0 and shell 4.0 long, radial divisions [800, 200, 200, 10], axial
+    100 (core) / 80 (shell), materials_synthetic.json, transient (erf) pulse
+    t_per 0.1, t_src 0.01, t_trs 1e-4, xi 4, zeta 2, I0 0.5742, S_C derived
+    from the domain (config.cpp:207), epsilon 1e-6, max_iter 10, the other
+    solver settings at their defaults (tau 1e-7 in the transient windows,
+    1e-4 elsewhere). Units as the reference's config (dimensionless Joule
+    factor I0^2 / S_C)."""
+    d = DomainSpec([0.24, 0.245, 0.25, 0.2501], 5.0, 4.0,
+                   ["copper_like", "insulator_like", "graphite_like", "coating_like"], 2)
+    timing = SourceSpec(t_per=0.1, t_src=0.01, t_trs=1e-4, xi=4.0, zeta=2.0, I0=0.5742,
+                        S_C=d.source_cross_section(), waveform=Waveform.Transient)
+    return Case("paper_cell", d, GridSpec([800, 200, 200, 10], 100, 80), synthetic_materials(),
+                timing, SolverConfig(epsilon=1e-6, max_iter=10), steps=steps,
+                notes="the reference's paper_cell.json")
+
+
+def small_paper(materials: str = "synthetic", I0: float = 0.0) -> Case:
+    """The acceptance suite's paper cell coarsened to 64 x 32
+    (acceptance_main.cpp:64-103): small_paper_domain, small_paper_gridspec,
+    paper_timing(I0); materials_synthetic.json or constant_materials()."""
+    d = DomainSpec([0.24, 0.245, 0.25, 0.2501], 5.0, 4.0, ["core", "ins", "heat", "coat"], 2)
+    if materials == "synthetic":
+        mats = synthetic_materials()
+    else:
+        def lin(v):
+            return PropertyTable([0.0, 400.0], [v, v])
+        mats = [MaterialTable("core", 2.0, lin(1.0), lin(2.0)),
+                MaterialTable("ins", 1.0, lin(0.8), lin(0.5), lin(2.0)),
+                MaterialTable("heat", 1.0, lin(1.2), lin(1.0), lin(2.0)),
+                MaterialTable("coat", 1.5, lin(0.9), lin(0.8))]
+    timing = SourceSpec(t_per=0.1, t_src=0.01, t_trs=1e-4, xi=4.0, zeta=2.0, I0=I0,
+                        S_C=math.pi * (0.25 * 0.25 - 0.245 * 0.245), waveform=Waveform.Transient)
+    return Case("small_paper", d, GridSpec([40, 8, 8, 8], 40, 24), mats, timing,
+                SolverConfig(), source_kind=SOURCE_NULL if I0 == 0.0 else SOURCE_JOULE)
+
+
 def make_source(case: Case, grid: Optional[Grid] = None):
     """The SourceModel a Case describes (JouleSource / NullSource / FieldSource)."""
     from .source import FieldSource, JouleSource, NullSource
@@ -186,4 +242,4 @@ def make_source(case: Case, grid: Optional[Grid] = None):
     return NullSource()
 
 
-CONFIGS = {"cfg0": cfg0, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4}
+CONFIGS = {"cfg0": cfg0, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4, "paper_cell": paper_cell}
