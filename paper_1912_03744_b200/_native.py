@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libpcgpu.so")
+# $PCGPU_LIB: another in-tree build of the library (A/B measurements)
+LIB_PATH = os.environ.get("PCGPU_LIB") or os.path.join(_HERE, "_lib", "libpcgpu.so")
 
 PCGPU_ABI_VERSION = 3
 DIST_IPC_BYTES = 256
