@@ -145,7 +145,10 @@ struct ResArgs {
 // Whether the resident stepper applies (exact-x / exact-lean lookups, no FIELD
 // source, <= kResProbes probes) and its grid size (0: not co-resident).
 int resident_grid(const DevProblem& P);
-void launch_resident(const DevProblem& P, const ResArgs& A, int grid, cudaStream_t s);
+// Whether that grid runs as a single thread-block cluster (<= 16 CTAs).
+bool resident_cluster(const DevProblem& P, int grid);
+void launch_resident(const DevProblem& P, const ResArgs& A, int grid, bool cluster,
+                     cudaStream_t s);
 
 // Selects `dev` for the scope of an entry point and restores the caller's
 // current device afterwards (the library never leaves the current device

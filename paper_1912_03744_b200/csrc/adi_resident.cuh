@@ -39,10 +39,22 @@ __device__ __forceinline__ void bar_k34() {  // warps 0-7 (K3 / K4 tiles)
   asm volatile("bar.sync 2, %0;" ::"n"(kT3Threads) : "memory");
 }
 
-template <int kX>
-__global__ void __launch_bounds__(kResThreads, 1) k_resident(DevProblem P, ResArgs A) {
+// kCluster: the whole grid is one thread-block cluster (at most 16 CTAs, one
+// GPC): the phase barrier is the hardware cluster barrier instead of the
+// cooperative grid barrier's global-memory atomics and polling (which cross
+// the two dies).
+template <int kX, bool kCluster>
+__global__ void __launch_bounds__(kResThreads, 1)
+    k_resident(const __grid_constant__ DevProblem P, const __grid_constant__ ResArgs A) {
   namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
+  struct PhaseBarrier {
+    __device__ void sync() const {
+      if (kCluster)
+        cg::this_cluster().sync();
+      else
+        cg::this_grid().sync();
+    }
+  } grid;
   extern __shared__ __align__(128) double sm[];
   const int tid = threadIdx.x;
   const bool lead = blockIdx.x == 0 && tid == 0;
@@ -55,7 +67,6 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(DevProblem P, ResAr
   int state = A.state0;
   int hs = 0;  // half-step counter: status buffers alternate
   double(*te)[kT3Rows + 1] = reinterpret_cast<double(*)[kT3Rows + 1]>(sm);
-  double(*tt)[kT3Rows + 1] = te + 32;
   // phase profile (lead thread only)
   unsigned long long t_last = 0;
   auto mark = [&](int phase) {
@@ -103,7 +114,7 @@ __global__ void __launch_bounds__(kResThreads, 1) k_resident(DevProblem P, ResAr
       DevStatus* st_next = A.st2 + (++hs & 1);
       if (tid < kT3Threads)  // K3: explicit_axial_pass (T_cur -> Lambda_z, T copy)
         for (int q = blockIdx.x; q < k3x * k3y; q += G) {
-          explicit_axial_t3_tile<kX>(P, cur, A.ExplT, A.TcT, st, q % k3x, q / k3x, tid, te, tt,
+          explicit_axial_t3_tile<kX>(P, cur, A.ExplT, A.TcT, st, q % k3x, q / k3x, tid, te, te + 32,
                                      bar_k34);
           bar_k34();
         }

@@ -224,6 +224,7 @@ struct pcgpu_stepper {
   // grid size (0: not applicable), device control block, schedule and log
   static constexpr int kResBatch = 1024;
   int res_grid = 0;
+  bool res_cluster = false;  // the resident grid is one thread-block cluster
   ResCtl* res_ctl = nullptr;       // device
   ResCtl* res_ctl_host = nullptr;  // pinned
   ResSched* res_sched = nullptr;   // device [kResBatch]
@@ -250,6 +251,20 @@ struct pcgpu_stepper {
       for (int q = 0; q < 6; ++q)
         std::fprintf(stderr, " %s %.2f us x %.0f;", names[q],
                      res_prof_n[q] ? res_prof_ns[q] / res_prof_n[q] / 1e3 : 0.0, res_prof_n[q]);
+      if (P.prof) {  // solver warp of line block 0: cycles per row waiting / in the chain
+        unsigned long long c[16] = {};
+        cudaMemcpy(c, P.prof, sizeof c, cudaMemcpyDeviceToHost);
+        std::fprintf(stderr, " solver cycles/row: radial wait %.1f chain %.1f, axial wait %.1f "
+                     "chain %.1f;", c[4] ? 1.0 * c[0] / c[4] : 0.0, c[4] ? 1.0 * c[1] / c[4] : 0.0,
+                     c[5] ? 1.0 * c[2] / c[5] : 0.0, c[5] ? 1.0 * c[3] / c[5] : 0.0);
+        // per call (cycles): entry -> forward, forward end -> back start, back pass
+        const double nr_ = res_prof_n[2] ? res_prof_n[2] : 1, na_ = res_prof_n[4] ? res_prof_n[4] : 1;
+        std::fprintf(stderr, " per call cycles: radial pre %.0f bulk %.0f back %.0f, axial pre %.0f "
+                     "bulk %.0f back %.0f;", c[6] / nr_, (1.0 * c[10] - c[8]) / nr_,
+                     (1.0 * c[12] - c[10]) / nr_, c[7] / na_, (1.0 * c[11] - c[9]) / na_,
+                     (1.0 * c[13] - c[11]) / na_);
+        std::fprintf(stderr, " back loop alone: radial %.0f axial %.0f;", c[14] / nr_, c[15] / na_);
+      }
       std::fprintf(stderr, "\n");
     }
     delete runner;
@@ -722,7 +737,7 @@ struct pcgpu_stepper {
       CK(cudaMemsetAsync(res_ctl->prof_ns, 0, sizeof(res_ctl->prof_ns), stream));
       CK(cudaMemsetAsync(res_ctl->prof_n, 0, sizeof(res_ctl->prof_n), stream));
     }
-    launch_resident(P, A, res_grid, stream);
+    launch_resident(P, A, res_grid, res_cluster, stream);
     CK(cudaMemcpyAsync(res_ctl_host, res_ctl, sizeof(ResCtl), cudaMemcpyDeviceToHost, stream));
     CK(cudaMemcpyAsync(res_log_host, res_log, sizeof(ResLog) * n, cudaMemcpyDeviceToHost,
                        stream));
@@ -1036,6 +1051,14 @@ void build_dev_problem(const pcgpu_desc* d, DevProblem& P, std::vector<void*>& a
     P.exact_ws = std::getenv("PCGPU_NO_EXACTWS") ? 0 : 1;
     // test knob: every full tile of the line solvers takes the reciprocal redo path
     P.rcp_redo = std::getenv("PCGPU_RCP_REDO") ? 1 : 0;
+    P.prof = nullptr;
+    if (std::getenv("PCGPU_RES_PROF")) {  // solver-warp cycle counters (resident profile)
+      unsigned long long* pc = nullptr;
+      CK(cudaMalloc(&pc, sizeof(unsigned long long) * 16));
+      CK(cudaMemset(pc, 0, sizeof(unsigned long long) * 16));
+      allocs.push_back(pc);
+      P.prof = pc;
+    }
     P.nr = nr;
     P.nz = nz;
     P.nr_core = d->nr_core;
@@ -1201,6 +1224,7 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
     // the resident stepper where it applies ($PCGPU_RESIDENT=0: host-driven steps)
     const char* rv = std::getenv("PCGPU_RESIDENT");
     h->res_grid = (rv && std::atoi(rv) == 0) ? 0 : resident_grid(h->P);
+    h->res_cluster = h->res_grid > 0 && resident_cluster(h->P, h->res_grid);
     h->launches0 = g_launches;
   } catch (const CudaError& ce) {
     g_create_error = std::string(ce.what) + ": " + cudaGetErrorString(ce.e);
@@ -1265,6 +1289,10 @@ int32_t pcgpu_describe(const pcgpu_stepper* h, char* buf, int32_t len) {
   s += h->P.exact_ws ? "ws" : "thread";
   s += " lookups=";
   s += h->P.exact_lean ? "exact-lean" : (h->P.exact_x ? "exact-x" : "generic");
+  s += " steps=";
+  s += h->res_grid ? (std::string("resident:") + std::to_string(h->res_grid) +
+                      (h->res_cluster ? "-cta-cluster" : "-cta-cooperative"))
+                   : std::string("host-driven");
   if (buf && len > 0) {
     const size_t n = std::min(s.size(), static_cast<size_t>(len - 1));
     std::memcpy(buf, s.data(), n);

@@ -362,7 +362,7 @@ def test_field_source_exact_lookups_half_steps_bitwise(cuda, kind, monkeypatch):
     g = case.grid()
     src = _Manufactured(g)
     gpu = gpu_stepper(case, "exact", src)
-    assert gpu.describe().endswith(kind)
+    assert f"lookups={kind} " in gpu.describe()
     port = PortStepper(case)
     f = configs.smooth_field(g, 10.0)
     t, tau = 0.01, 1e-5
@@ -651,7 +651,7 @@ def _cfg4s():
 
 def test_exact_selects_ws_and_exact_x_for_configs(cuda):
     gpu = gpu_stepper(_cfg4s(), "exact")
-    assert gpu.describe() == "mode=exact lines=ws lookups=exact-lean"
+    assert gpu.describe().startswith("mode=exact lines=ws lookups=exact-lean steps=resident:")
     gpu = gpu_stepper(configs.step_cell(True), "exact")
     assert gpu.describe().startswith("mode=exact lines=ws")
 
@@ -678,7 +678,7 @@ def test_exact_x_out_of_range_clamp_events_bitwise(cuda, lookup_kind):
     f[50:52, 5:7] = 3.95
     f[63, 40] = 3.97
     port, gpu = PortStepper(case), gpu_stepper(case, "exact")
-    assert gpu.describe().endswith("lookups=" + lookup_kind)
+    assert f"lookups={lookup_kind} " in gpu.describe()
     fo = f.copy(order="F")
     te_o, _, res_o = port.run(fo, 0.0, 6)
     fg = to_dev(f)
