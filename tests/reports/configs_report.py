@@ -1,17 +1,21 @@
 """TEST INFRASTRUCTURE (a report, not a test): every BASELINE.json config on one B200, next to the reference's own CPU path
 on the same box's host cores. Prints one JSON object; the
-committed copy lives in profiles/ (r01_configs_report.json).
+committed copies live in profiles/ (r0N_configs_report.json).
 
   cfg0  100 x 200, tau 1e-4, 2000 steps: the whole run on the GPU (pcgpu_run)
-        and the whole run through the reference's AdiStepper on all host
-        cores; final fields compared bit for bit.
+        -- the resident stepper (one launch) and the host-driven path -- and
+        the whole run through the reference's AdiStepper on all host cores;
+        final fields compared bit for bit.
+  paper the reference's own paper_cell.json (1210 x 100, transient pulse),
+        3000 steps on the GPU and through the reference, bit for bit.
   cfg1  131072 x 1024 batched Thomas, both layouts (tools/bench_tridiag.py);
         the reference's thomas_solve_inplace over a bounded sample of systems
         on all host cores.
   cfg2  1024 x 2048, BASELINE growth controller, 5 pulse periods on the GPU;
         the first steps checked bit for bit against the C restatement's
-        controller (oracle_run_growth); the reference AdiStepper timed on a
-        bounded number of steps (its own tau controller) on all host cores.
+        controller (the whole run against the reference's own half-steps is
+        adaptive_full_parity.py); the reference AdiStepper timed on a bounded
+        number of steps (its own tau controller) on all host cores.
   cfg4  2048 x 4096 stepped cell, growth controller, 10 periods; same checks.
 cfg3 is bench.py's workload.
 
@@ -64,9 +68,10 @@ def _ref_rate(case, steps, t0=0.0):
                       "cell-updates, the reference's own tau controller)"}
 
 
-def cfg0():
-    from oracle.oracle import RefStepper
-    case = configs.cfg0()
+def _fixed_run(case, path):
+    """The whole fixed-dt run on the GPU: `path` "resident" (one cooperative /
+    cluster launch per batch) or "host" (host-driven Picard batches)."""
+    os.environ["PCGPU_RESIDENT"] = "1" if path == "resident" else "0"
     g = case.grid()
     st = _gpu_stepper(case, g)
     f = _dev_field(g, case.solver.T0)
@@ -76,6 +81,16 @@ def cfg0():
     t_end, stats, _ = st.run(f, 0.0, case.steps)
     torch.cuda.synchronize()
     dt = time.perf_counter() - s0
+    os.environ.pop("PCGPU_RESIDENT")
+    return f, t_end, stats, dt, st.describe(), st.launch_count()
+
+
+def cfg0(case=None, sample="the whole 2000-step run"):
+    from oracle.oracle import RefStepper
+    case = case or configs.cfg0()
+    g = case.grid()
+    fh, _, hstats, hdt, hdesc, _ = _fixed_run(case, "host")
+    f, t_end, stats, dt, desc, launches = _fixed_run(case, "resident")
     ref = RefStepper(case, workers=CORES)
     fr = make_field(g, case.solver.T0)
     r0 = time.perf_counter()
@@ -83,15 +98,20 @@ def cfg0():
     rdt = time.perf_counter() - r0
     m = g.mask()
     same = bool(np.array_equal(_host(f)[m], fr[m]))
+    same_host = bool(np.array_equal(_host(fh)[m], fr[m]))
     return {"grid": f"{g.nr()}x{g.nz()}", "steps": case.steps, "t_end": t_end,
             "gpu": {"seconds": dt, "cell_updates": stats["cell_updates"],
                     "value": stats["cell_updates"] / dt, "unit": "cell-updates/s",
                     "radial_iters": stats["radial_iterations"],
                     "axial_iters": stats["axial_iterations"], "halvings": stats["halvings"],
-                    "timing": "wall clock around pcgpu_run (launch-bound grid)"},
+                    "kernels": desc, "kernel_launches": launches,
+                    "timing": "wall clock around pcgpu_run (resident stepper)"},
+            "gpu_host_driven": {"seconds": hdt, "value": hstats["cell_updates"] / hdt,
+                                "unit": "cell-updates/s", "kernels": hdesc,
+                                "final_field_bitwise_vs_reference": same_host},
             "cpu_reference": {"seconds": rdt, "value": rstats["cell_updates"] / rdt,
                               "unit": "cell-updates/s", "cores": CORES, "kind": "reference",
-                              "sample": "the whole 2000-step run"},
+                              "sample": sample},
             "parity": {"final_field_bitwise_vs_reference": same,
                        "iterations_equal": (rstats["radial_iterations"],
                                             rstats["axial_iterations"]) ==
@@ -100,18 +120,11 @@ def cfg0():
 
 
 def cfg1(cpu_systems=16384):
-    from tools.bench_tridiag import run
+    from tools.bench_tridiag import generate, run
     from oracle.oracle import ref_thomas_batch
     gpu = run(check=256)
-    rng = np.random.default_rng(2024)
     n = 1024
-    a = -rng.random((cpu_systems, n))
-    c = -rng.random((cpu_systems, n))
-    a[:, 0] = 0.0
-    c[:, -1] = 0.0
-    b = 2.05 + np.abs(a) + np.abs(c)
-    d = rng.random((cpu_systems, n)) * 2 - 1
-    bands = [np.ascontiguousarray(v).ravel() for v in (a, b, c, d)]
+    bands = [v.ravel() for v in generate(cpu_systems, n)]  # std::mt19937_64(2024)
     ref_thomas_batch(*bands, n, cpu_systems, 0, workers=CORES)  # warm-up
     s0 = time.perf_counter()
     ref_thomas_batch(*bands, n, cpu_systems, 0, workers=CORES)
@@ -159,13 +172,15 @@ def _growth_case(case, check_steps, cpu_steps):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="cfg0,cfg1,cfg2,cfg4")
+    ap.add_argument("--only", default="cfg0,paper,cfg1,cfg2,cfg4")
     ap.add_argument("--periods-scale", type=float, default=1.0)
     a = ap.parse_args()
     out = {"device": torch.cuda.get_device_name(0), "host_cores": CORES}
     want = a.only.split(",")
     if "cfg0" in want:
         out["cfg0"] = cfg0()
+    if "paper" in want:
+        out["paper_cell"] = cfg0(configs.paper_cell(3000), "the whole 3000-step run")
     if "cfg1" in want:
         out["cfg1"] = cfg1()
     if "cfg2" in want:
