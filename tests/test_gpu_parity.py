@@ -393,6 +393,54 @@ def test_tridiag_batch_exact_bitwise(cuda, layout):
     assert np.array_equal(got, want)
 
 
+def test_tridiag_cfg1_full_size_vs_reference(cuda):
+    """configs[1] in full -- 131072 systems of length 1024 drawn from
+    std::mt19937_64(2024) as SURVEY 8(d) specifies -- in both layouts, every
+    system bit for bit against the reference's own thomas_solve_inplace over a
+    LinePool of all host cores (the C restatement without the reference)."""
+    import torch
+    from oracle.oracle import port_thomas_batch, ref_available, ref_thomas_batch
+    from paper_1912_03744_b200.tridiagonal import CONTIGUOUS, STRIDED, thomas_solve_batch
+    from tools.bench_tridiag import generate
+    batch, n = 131072, 1024
+    a, b, c, d = generate(batch, n)
+    bands = [v.ravel() for v in (a, b, c, d)]
+    if ref_available():
+        rc, want, _ = ref_thomas_batch(*bands, n, batch, 0, workers=os.cpu_count() or 1)
+    else:
+        rc, want, _ = port_thomas_batch(*bands, n, batch, 0)
+    assert rc == 0
+    want = want.reshape(batch, n)
+    for layout in (CONTIGUOUS, STRIDED):
+        host = (a, b, c, d) if layout == CONTIGUOUS else tuple(v.T for v in (a, b, c, d))
+        dev = [torch.from_numpy(np.ascontiguousarray(v)).cuda().view(-1) for v in host]
+        x = torch.empty_like(dev[3])
+        thomas_solve_batch(*dev, x, n, batch, layout)
+        got = x.view(batch, n) if layout == CONTIGUOUS else x.view(n, batch).t()
+        assert np.array_equal(got.cpu().numpy(), want), layout
+        del dev, x
+        torch.cuda.empty_cache()
+
+
+def test_tridiag_batch_rejects_bad_tensors(cuda):
+    """The binding validates dtype, contiguity, size and device before any
+    pointer reaches the kernels (an out-of-bounds write otherwise)."""
+    import torch
+    from paper_1912_03744_b200.tridiagonal import thomas_solve_batch
+    n, batch = 8, 4
+    ok = [torch.ones(n * batch, dtype=torch.float64, device="cuda") for _ in range(5)]
+    bad_dtype = ok[:3] + [ok[3].float(), ok[4]]
+    with pytest.raises(ValueError):
+        thomas_solve_batch(*bad_dtype, n, batch)
+    strided = torch.ones(2 * n * batch, dtype=torch.float64, device="cuda")[::2]
+    with pytest.raises(ValueError):
+        thomas_solve_batch(*ok[:4], strided, n, batch)
+    with pytest.raises(ValueError):
+        thomas_solve_batch(*ok[:4], ok[4][:-1], n, batch)
+    with pytest.raises(ValueError):
+        thomas_solve_batch(*ok[:4], ok[4].cpu(), n, batch)
+
+
 @pytest.mark.parametrize("n,batch", [(2, 1), (16, 32), (30, 33), (1024, 200), (1000, 97),
                                      (7, 40)])
 def test_tridiag_batch_contiguous_fused_ragged(cuda, n, batch):
