@@ -226,6 +226,9 @@ def main():
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     launches = stepper.launch_count() - launches0
+    # how the steps were driven: speculative batches (one host read per batch)
+    # on this grid; the resident stepper on grids of <= one line block per SM
+    spec = {"speculative": stepper.speculation_stats(), "resident": stepper.resident_stats()}
     kernels_desc = stepper.describe()
     kt = stepper.kernel_timing()
     stepper.enable_kernel_timing(False)
@@ -355,7 +358,8 @@ def main():
                            l2="inputs > L2 (1 GiB FP64 fields)",
                            picard={"radial_iters": stats["radial_iterations"],
                                    "axial_iters": stats["axial_iterations"],
-                                   "halvings": stats["halvings"], "steps": stats["steps"]}),
+                                   "halvings": stats["halvings"], "steps": stats["steps"]},
+                           controller=spec),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_unit": "GB per launch (ncu dram__bytes_read+write)",

@@ -206,6 +206,15 @@ int pcgpu_last_tau_floor(const pcgpu_stepper* h, double* tau, double* floor, dou
  * steps they accepted, steps redone host-driven (> 8 halvings in one step). */
 int pcgpu_resident_stats(const pcgpu_stepper* h, int32_t* grid, int64_t* batches, int64_t* steps,
                          int64_t* host_steps);
+/* Host-driven runs (grids the resident stepper does not take, e.g. configs[3];
+ * pcgpu_run / pcgpu_run_growth): batches of steps enqueued with the predicted
+ * Picard counts and no host read inside a batch, verified by one read at its
+ * end; a misprediction, halving or error undoes the batch (its input field is
+ * never written; clamp counters restored) and replays it step by step
+ * ($PCGPU_NO_SPECULATE=1: always step by step). Batches, steps they accepted,
+ * batches undone. */
+int pcgpu_speculation_stats(const pcgpu_stepper* h, int64_t* batches, int64_t* steps,
+                            int64_t* rollbacks);
 
 /* Per-cell power for PCGPU_SOURCE_FIELD: device pointer, nr x nz column-major,
  * read by the next half-step (the SourceModel::power(i, j, ...) values for the

@@ -83,7 +83,8 @@ EXPORTS = [
     "pcgpu_abi_version", "pcgpu_device_count", "pcgpu_create", "pcgpu_destroy",
     "pcgpu_last_error", "pcgpu_error_line", "pcgpu_initial_tau", "pcgpu_pulse_value",
     "pcgpu_active_cells", "pcgpu_set_host_clock", "pcgpu_last_tau_floor",
-    "pcgpu_resident_stats", "pcgpu_bind_power_field", "pcgpu_radial_half_step",
+    "pcgpu_resident_stats", "pcgpu_speculation_stats", "pcgpu_bind_power_field",
+    "pcgpu_radial_half_step",
     "pcgpu_axial_half_step", "pcgpu_step", "pcgpu_step_host", "pcgpu_radial_half_step_host",
     "pcgpu_axial_half_step_host", "pcgpu_run", "pcgpu_clamp_events", "pcgpu_stream",
     "pcgpu_kernel_timing", "pcgpu_enable_kernel_timing", "pcgpu_launch_count",
@@ -130,6 +131,8 @@ def load():
                                            C.POINTER(C.c_double)]),
         "pcgpu_resident_stats": (C.c_int, [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int64),
                                            C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+        "pcgpu_speculation_stats": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                              C.POINTER(C.c_int64)]),
         "pcgpu_bind_power_field": (C.c_int, [vp, vp]),
         "pcgpu_radial_half_step": (C.c_int, [vp, vp, C.c_double, C.c_double, vp,
                                              C.POINTER(Outcome)]),

@@ -13,10 +13,22 @@ namespace pcgpu {
 
 // ---- exact mode (bit-identical to the reference; adi_exact.cu, --fmad=false) ----
 
+// Speculative batches (pcgpu.cu host_run): K3's / K4's source is the result
+// of the previous sweep, picked on the device by that sweep's convergence
+// count (odd / even iterate buffer); a half-step whose status carries
+// kSpecAbort is skipped whole. st == nullptr: the source pointer as given.
+struct SpecPick {
+  const DevStatus* st = nullptr;  // the sweep that produced the source
+  const double* odd = nullptr;    // its result after an odd count
+  const double* even = nullptr;   // ... after an even count
+  double eps = 0.0;
+};
+
 // K3 explicit_axial_pass (solver.cpp:162-189): explT = Lambda_z[srcN]; also
 // writes srcT = transpose(srcN) (the anchor for the T-layout radial sweep).
 void launch_explicit_axial_exact(const DevProblem& P, const double* srcN, double* explT,
-                                 double* srcT, DevStatus* st, cudaStream_t s);
+                                 double* srcT, DevStatus* st, cudaStream_t s,
+                                 const SpecPick& pick = SpecPick{});
 // K1 one Picard iteration of the radial sweep (solver.cpp:191-233, :245-248),
 // T layout, thread per radial line. Early-exits when iteration it-1 converged.
 void launch_radial_exact(const DevProblem& P, int it, double eps, double half_k, double pulse,
@@ -29,7 +41,8 @@ void launch_radial_exact(const DevProblem& P, int it, double eps, double half_k,
 // errors); the axial sweep then computes K-bar itself (kbar_on_the_fly).
 void launch_axial_rhs_exact(const DevProblem& P, double half_k, double pulse,
                             const double* halfT, const double* powN, double* kbarN,
-                            double* explN, double* halfN, DevStatus* st, cudaStream_t s);
+                            double* explN, double* halfN, DevStatus* st, cudaStream_t s,
+                            const SpecPick& pick = SpecPick{});
 // K2 one Picard iteration of the axial sweep (solver.cpp:286-332, :343-345),
 // N layout, thread per axial line. kbarN == nullptr (only when
 // kbar_on_the_fly(P)): K-bar = rho * c_V(ThN) * half_k inside the sweep.

@@ -146,6 +146,40 @@ void launch_add_counters(unsigned long long* dst, const unsigned long long* slot
   k_add_counters<<<1, 32, 0, s>>>(dst, slots, n, stride, nslots);
 }
 
+// Speculative batches (pcgpu_stepper::host_run). Reset: every status of the
+// batch cleared, the clamp counters snapshot taken.
+__global__ void k_spec_reset(DevStatus* st, int n, const unsigned long long* clamp,
+                             unsigned long long* save, int n_layers) {
+  for (int q = threadIdx.x; q < n; q += blockDim.x) {
+    for (int it = 0; it <= kMaxIter; ++it) st[q].delta[it] = 0;
+    st[q].err = kNoError;
+  }
+  if (threadIdx.x < n_layers) save[threadIdx.x] = clamp[threadIdx.x];
+}
+// Verify one half-step: it must have converged within its `launched`
+// iterations without error; otherwise every later half-step of the batch is
+// marked kSpecAbort (its kernels return at once, so the field it started from
+// survives). `snapshot`: after a passing axial sweep, the clamp counters of the
+// completed step become the restore point.
+__global__ void k_spec_verify(const DevStatus* st, int launched, double eps, DevStatus* later,
+                              int n_later, const unsigned long long* clamp,
+                              unsigned long long* save, int n_layers, int snapshot) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    int conv = 0;
+    if (st->err == kNoError)
+      for (int it = 1; it <= launched && !conv; ++it)
+        conv = __longlong_as_double(static_cast<long long>(st->delta[it])) < eps;
+    ok = st->err == kSpecAbort ? 2 : conv;  // 2: aborted upstream, already marked
+  }
+  __syncthreads();
+  if (ok == 0) {
+    for (int q = threadIdx.x; q < n_later; q += blockDim.x) later[q].err = kSpecAbort;
+  } else if (ok == 1 && snapshot && threadIdx.x < n_layers) {
+    save[threadIdx.x] = clamp[threadIdx.x];
+  }
+}
+
 template <typename T>
 T* dev_upload(const std::vector<T>& v) {
   T* p = nullptr;
@@ -200,7 +234,7 @@ struct pcgpu_stepper {
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
-  struct Timed { cudaEvent_t a, b; int sweep; int it; };
+  struct Timed { cudaEvent_t a, b; int sweep; int it; int tag; };  // tag: batch step + 1
   std::vector<Timed> pending;
   double radial_ms = 0, axial_ms = 0;
   int64_t radial_launches = 0, axial_launches = 0;
@@ -357,18 +391,19 @@ struct pcgpu_stepper {
     (void)sweep;
     (void)it;
   }
-  void timed_end(int sweep, int it, cudaEvent_t a) {
+  void timed_end(int sweep, int it, cudaEvent_t a, int tag = 0) {
     if (!timing) return;
     cudaEvent_t b = event();
     CK(cudaEventRecord(b, stream));
-    pending.push_back({a, b, sweep, it});
+    pending.push_back({a, b, sweep, it, tag});
   }
-  // After a sync: accumulate the durations of the iterations that ran.
-  void collect_timing(int sweep, int ran) {
+  // After a sync: accumulate the durations of the iterations that ran (of
+  // one sweep; tag < 0: every tag, else that batch step only).
+  void collect_timing(int sweep, int ran, int tag = -1) {
     if (!timing) return;
     std::vector<Timed> keep;
     for (const Timed& t : pending) {
-      if (t.sweep != sweep) { keep.push_back(t); continue; }
+      if (t.sweep != sweep || (tag >= 0 && t.tag != tag)) { keep.push_back(t); continue; }
       if (t.it <= ran) {
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, t.a, t.b));
@@ -378,6 +413,10 @@ struct pcgpu_stepper {
     }
     pending.swap(keep);
     if (pending.empty()) ev_used = 0;
+  }
+  void drop_timing() {
+    pending.clear();
+    ev_used = 0;
   }
 
   // ---- Picard loop driver shared by both sweeps ----------------------------
@@ -866,6 +905,232 @@ struct pcgpu_stepper {
     CK(cudaStreamSynchronize(stream));
   }
   double fail_tau = 0, fail_t = 0;
+
+  // ---- speculative batches (grids too large for the resident stepper) -------
+  // Host-driven runs read a status after every half-step. The Picard counts
+  // of consecutive steps are nearly constant on the large grids, so instead a
+  // batch of up to kSpecBatch steps is enqueued at once: each with its tau
+  // from the schedule (no halving), each sweep launching its predicted count
+  // + 1 iterations (those after convergence return at once, as in the
+  // host-driven sweep). The iterate a sweep converged in depends on the count's
+  // parity, so the next kernel (K4 after the radial sweep, the next step's K3
+  // after the axial one) picks it on the device (SpecPick). A one-thread
+  // verify kernel after each sweep checks convergence within the launched
+  // count without error; on failure every later half-step is marked
+  // kSpecAbort and does nothing. Steps alternate between two pairs of
+  // iterate buffers, so the field a failed step started from is intact: the
+  // steps before it are kept, the clamp counters go back to the snapshot
+  // taken after the last good step, and that step is redone host-driven
+  // (halving, error, longer sweep). One read per batch. Same kernels, same
+  // arithmetic: bit-identical to the step-by-step path.
+  static constexpr int kSpecBatch = 16;
+  double* spec_n[4] = {};            // two pairs of N-layout iterate buffers
+  bool spec_alloc_failed = false;
+  DevStatus* spec_st = nullptr;      // [2 * kSpecBatch] status per half-step
+  DevStatus* spec_st_host = nullptr;
+  unsigned long long* spec_clamp_save = nullptr;  // [kMaxLayers]
+  int64_t spec_batches = 0, spec_steps = 0, spec_rollbacks = 0;
+  bool spec_ok() const {
+    return P.exact_ws && d.source_kind != PCGPU_SOURCE_FIELD && !spec_alloc_failed &&
+           std::getenv("PCGPU_NO_SPECULATE") == nullptr;
+  }
+  bool spec_ready() {
+    if (spec_st) return true;
+    if (spec_alloc_failed) return false;
+    for (int q = 0; q < 4; ++q) {  // disjoint from buf[kField] / kNext / kIterT
+      if (cudaMalloc(&spec_n[q], sizeof(double) * cells()) != cudaSuccess) {
+        cudaGetLastError();  // not enough memory: run step by step
+        for (int r = 0; r < q; ++r) cudaFree(spec_n[r]);
+        for (auto& p : spec_n) p = nullptr;
+        spec_alloc_failed = true;
+        return false;
+      }
+    }
+    for (double* p : spec_n) dev_allocs.push_back(p);
+    CK(cudaMalloc(&spec_st, sizeof(DevStatus) * 2 * kSpecBatch));
+    dev_allocs.push_back(spec_st);
+    CK(cudaMallocHost(&spec_st_host, sizeof(DevStatus) * 2 * kSpecBatch));
+    CK(cudaMalloc(&spec_clamp_save, sizeof(unsigned long long) * kMaxLayers));
+    dev_allocs.push_back(spec_clamp_save);
+    return true;
+  }
+
+  // Step k of a batch (statuses spec_st[2k], [2k+1]; n steps in all), from
+  // `from` (the previous step's SpecPick; from.st == nullptr: the field C)
+  // into the pair (Po, Qo): its result is Po after an odd axial count, Qo
+  // after an even one. Lr / La: iterations launched per sweep.
+  void spec_enqueue(int k, int n, const double* C, const SpecPick& from, double t, double tau,
+                    int Lr, int La, double* Po, double* Qo) {
+    const double pulse = pulse_for(t, tau);
+    const double hk = 2.0 / tau;
+    DevStatus* sr = spec_st + 2 * k;
+    DevStatus* sa = sr + 1;
+    const int nlater = 2 * (n - k);  // statuses after sr (sa included)
+    launch_explicit_axial_exact(P, C, buf[kExpl], buf[kTcT], sr, stream, from);
+    for (int it = 1; it <= Lr; ++it) {
+      const double* src = it == 1 ? buf[kTcT] : (it % 2 == 0 ? buf[kHalfT] : buf[kIterT]);
+      double* dst = it % 2 == 1 ? buf[kHalfT] : buf[kIterT];
+      cudaEvent_t a = nullptr;
+      timed_begin(0, it, &a);
+      launch_radial_exact(P, it, d.epsilon, hk, pulse, src, buf[kTcT], buf[kExpl], buf[kPowT], dst,
+                          buf[kW], buf[kX], sr, stream);
+      timed_end(0, it, a, k + 1);
+    }
+    k_spec_verify<<<1, 32, 0, stream>>>(sr, Lr, d.epsilon, sa, nlater - 1, P.clamp,
+                                        spec_clamp_save, d.n_layers, 0);
+    SpecPick half;
+    half.st = sr;
+    half.odd = buf[kHalfT];
+    half.even = buf[kIterT];
+    half.eps = d.epsilon;
+    double* kbar = kbar_on_the_fly(P) ? nullptr : buf[kKbar];
+    double* anchor = buf[kTcT];  // halfN
+    launch_axial_rhs_exact(P, hk, pulse, nullptr, buf[kPowN], kbar, buf[kExpl], anchor, sa, stream,
+                           half);
+    for (int it = 1; it <= La; ++it) {
+      const double* src = it == 1 ? anchor : (it % 2 == 0 ? Po : Qo);
+      double* dst = it % 2 == 1 ? Po : Qo;
+      cudaEvent_t a = nullptr;
+      timed_begin(1, it, &a);
+      launch_axial_exact(P, it, d.epsilon, hk, src, anchor, kbar, buf[kExpl], dst, buf[kW],
+                         buf[kX], sa, stream);
+      timed_end(1, it, a, k + 1);
+    }
+    k_spec_verify<<<1, 32, 0, stream>>>(sa, La, d.epsilon, sa + 1, nlater - 2, P.clamp,
+                                        spec_clamp_save, d.n_layers, 1);
+    g_launches += 2;
+  }
+
+  // First converged iteration (<= launched) of a batch status, no error; 0 if none.
+  int spec_conv(const DevStatus& x, int launched, double* last) const {
+    if (x.err != kNoError) return 0;
+    for (int it = 1; it <= launched; ++it) {
+      double dl;
+      std::memcpy(&dl, &x.delta[it], sizeof dl);
+      if (dl < d.epsilon) {
+        *last = dl;
+        return it;
+      }
+    }
+    return 0;
+  }
+
+  // Host-driven runs: speculative batches, each failed step redone step by
+  // step. The field is buf[kField] in and out. Plan / accept / more as in
+  // res_run.
+  template <typename Plan, typename Accept, typename More>
+  int host_run(double* t, int64_t max_steps, Plan&& plan, Accept&& accept, More&& more,
+               pcgpu_step_result* results, pcgpu_run_stats* s) {
+    int64_t done = 0;
+    auto record = [&](const pcgpu_step_result& r, double upd) {
+      *t += r.tau_used;
+      if (results) results[done] = r;
+      s->steps += 1;
+      s->halvings += r.halvings;
+      s->radial_iterations += r.radial.iterations;
+      s->axial_iterations += r.axial.iterations;
+      s->cell_updates += upd;
+      s->cell_updates_accepted +=
+          static_cast<double>(active) * (r.radial.iterations + r.axial.iterations);
+      s->attempt_cells += 2.0 * static_cast<double>(active) * (r.halvings + 1);
+      accept(r);
+      ++done;
+    };
+    // one host-driven step of the field in buf[kField] (rotating kNext / kIterT)
+    auto safe_step = [&]() -> int {
+      pcgpu_step_result r;
+      const double* acc = nullptr;
+      double upd = 0;
+      double* cur = buf[kField];
+      const int rc = step(cur, *t, buf[kNext], &acc, &r, &upd, plan.next(plan.state(), *t));
+      if (rc) return rc;
+      double* accepted = const_cast<double*>(acc);
+      if (accepted == buf[kNext]) std::swap(buf[kField], buf[kNext]);
+      else std::swap(buf[kField], buf[kIterT]);
+      record(r, upd);
+      return PCGPU_OK;
+    };
+    bool learned = false;  // counts known from a host-driven step
+    while (done < max_steps && more(*t)) {
+      if (!learned || !spec_ok() || !spec_ready()) {
+        const int rc = safe_step();
+        if (rc) return rc;
+        learned = true;
+        continue;
+      }
+      const int Lr = std::min(d.max_iter, std::max(1, pred_radial) + 1);
+      const int La = std::min(d.max_iter, std::max(1, pred_axial) + 1);
+      int n = 0;
+      double tt = *t;
+      auto ps = plan.state();
+      double taus[kSpecBatch];
+      while (n < kSpecBatch && done + n < max_steps && (n == 0 || more(tt))) {
+        taus[n] = plan.next(ps, tt);
+        plan.advance(ps, taus[n]);
+        tt += taus[n];
+        ++n;
+      }
+      double* const C = buf[kField];  // the batch input: never written in the batch
+      k_spec_reset<<<1, 32, 0, stream>>>(spec_st, 2 * n, P.clamp, spec_clamp_save, d.n_layers);
+      ++g_launches;
+      SpecPick from;  // step 0 reads C
+      double ts = *t;
+      for (int k = 0; k < n; ++k) {
+        double* Po = spec_n[2 * (k & 1)];
+        double* Qo = spec_n[2 * (k & 1) + 1];
+        spec_enqueue(k, n, C, from, ts, taus[k], Lr, La, Po, Qo);
+        from.st = spec_st + 2 * k + 1;
+        from.odd = Po;
+        from.even = Qo;
+        from.eps = d.epsilon;
+        ts += taus[k];
+      }
+      CK(cudaMemcpyAsync(spec_st_host, spec_st, sizeof(DevStatus) * 2 * n, cudaMemcpyDeviceToHost,
+                         stream));
+      CK(cudaStreamSynchronize(stream));
+      ++spec_batches;
+      // the steps that converged within their launches, in order
+      int good = 0;
+      int q = -1;  // index in spec_n of the last good step's result
+      for (int k = 0; k < n; ++k) {
+        double dr = 0, da = 0;
+        const int cr = spec_conv(spec_st_host[2 * k], Lr, &dr);
+        const int ca = cr ? spec_conv(spec_st_host[2 * k + 1], La, &da) : 0;
+        if (!ca) break;
+        if (timing) {
+          collect_timing(0, cr, k + 1);
+          collect_timing(1, ca, k + 1);
+        }
+        pcgpu_step_result r{};
+        r.tau_used = taus[k];
+        r.radial = pcgpu_outcome{1, cr, dr};
+        r.axial = pcgpu_outcome{1, ca, da};
+        record(r, static_cast<double>(active) * (cr + ca));
+        pred_radial = cr;
+        pred_axial = ca;
+        q = 2 * (k & 1) + ((ca & 1) ? 0 : 1);
+        ++good;
+      }
+      if (timing) drop_timing();  // the failed step's launches are redone
+      spec_steps += good;
+      if (q >= 0) {  // the result becomes the field; the old field takes its place
+        buf[kField] = spec_n[q];
+        spec_n[q] = C;
+      }
+      if (good < n) {
+        // a sweep did not converge within its launches (or failed): redo that
+        // step host-driven from the counters after the last good step
+        ++spec_rollbacks;
+        CK(cudaMemcpyAsync(P.clamp, spec_clamp_save, sizeof(unsigned long long) * d.n_layers,
+                           cudaMemcpyDeviceToDevice, stream));
+        if (done < max_steps && more(*t)) {
+          const int rc = safe_step();
+          if (rc) return rc;
+        }
+      }
+    }
+    return PCGPU_OK;
+  }
 };
 
 // Schedules for the resident stepper's controller (pcgpu_stepper::res_run).
@@ -1225,6 +1490,8 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
     const char* rv = std::getenv("PCGPU_RESIDENT");
     h->res_grid = (rv && std::atoi(rv) == 0) ? 0 : resident_grid(h->P);
     h->res_cluster = h->res_grid > 0 && resident_cluster(h->P, h->res_grid);
+    // the speculative batches' buffers up front (not inside a timed run)
+    if (!h->res_grid && h->spec_ok()) h->spec_ready();  // outside any timed region
     h->launches0 = g_launches;
   } catch (const CudaError& ce) {
     g_create_error = std::string(ce.what) + ": " + cudaGetErrorString(ce.e);
@@ -1266,6 +1533,15 @@ int pcgpu_last_tau_floor(const pcgpu_stepper* h, double* tau, double* floor, dou
   *tau = h->fail_tau;
   *floor = h->tau_floor;
   *t = h->fail_t;
+  return PCGPU_OK;
+}
+
+int pcgpu_speculation_stats(const pcgpu_stepper* h, int64_t* batches, int64_t* steps,
+                            int64_t* rollbacks) {
+  if (!h || !batches || !steps || !rollbacks) return PCGPU_ERR_ARG;
+  *batches = h->spec_batches;
+  *steps = h->spec_steps;
+  *rollbacks = h->spec_rollbacks;
   return PCGPU_OK;
 }
 
@@ -1411,42 +1687,11 @@ int pcgpu_run(pcgpu_stepper* h, double* field, double t0, int32_t nsteps,
     return rc;
   }
   GUARD_BEGIN
-  // Resident field: rotate buffer roles instead of copying per step.
-  double* cur = h->buf[kField];
-  double* nxt = h->buf[kNext];
-  double* spare = h->buf[kIterT];
-  h->to_state(field, cur);
-  for (int32_t k = 0; k < nsteps; ++k) {
-    pcgpu_step_result r;
-    const double* acc = nullptr;
-    double upd = 0;
-    h->buf[kIterT] = spare;
-    rc = h->step(cur, t, nxt, &acc, &r, &upd);
-    if (rc) break;
-    t += r.tau_used;
-    if (results) results[k] = r;
-    s.steps += 1;
-    s.halvings += r.halvings;
-    s.radial_iterations += r.radial.iterations;
-    s.axial_iterations += r.axial.iterations;
-    s.cell_updates += upd;
-    s.cell_updates_accepted +=
-        static_cast<double>(h->active) * (r.radial.iterations + r.axial.iterations);
-    s.attempt_cells += 2.0 * static_cast<double>(h->active) * (r.halvings + 1);
-    // The accepted buffer becomes the field; the old field becomes scratch.
-    double* accepted = const_cast<double*>(acc);
-    double* old = cur;
-    cur = accepted;
-    if (accepted == nxt) {
-      nxt = old;
-    } else {
-      spare = old;
-    }
-  }
-  h->buf[kField] = cur;
-  h->buf[kNext] = nxt;
-  h->buf[kIterT] = spare;
-  h->from_state(cur, field);
+  // the field stays resident in buf[kField] (buffer roles rotate, no copies)
+  h->to_state(field, h->buf[kField]);
+  rc = h->host_run(&t, nsteps, FixedPlan{h}, [](const pcgpu_step_result&) {},
+                   [](double) { return true; }, results, &s);
+  h->from_state(h->buf[kField], field);
   CK(cudaStreamSynchronize(h->stream));
   GUARD_END(h)
   s.t_end = t;
@@ -1454,13 +1699,6 @@ int pcgpu_run(pcgpu_stepper* h, double* field, double t0, int32_t nsteps,
   return rc;
 }
 
-// The BASELINE adaptive policy (configs[2], configs[4]) as a controller
-// above step(): start at tau_start; a step that needs halving (a Picard sweep
-// did not converge within max_iter) retries at tau/2 like the reference
-// (solver.cpp:369-371); after `easy_steps` consecutive steps accepted without
-// halving, tau grows by `grow`; tau never exceeds tau_max. The reference has
-// no growth logic; the policy is shared with the CPU oracle so
-// both see the same decisions.
 int pcgpu_run_growth(pcgpu_stepper* h, double* field, double t0, double t_end, int32_t max_steps,
                      double tau_start, double grow, int32_t easy_steps, double tau_max,
                      pcgpu_step_result* results, pcgpu_run_stats* stats) {
@@ -1484,43 +1722,13 @@ int pcgpu_run_growth(pcgpu_stepper* h, double* field, double t0, double t_end, i
     return rc;
   }
   GUARD_BEGIN
-  double* cur = h->buf[kField];
-  double* nxt = h->buf[kNext];
-  double* spare = h->buf[kIterT];
-  h->to_state(field, cur);
-  for (int32_t k = 0; k < max_steps && t < t_end; ++k) {
-    pcgpu_step_result r;
-    const double* acc = nullptr;
-    double upd = 0;
-    h->buf[kIterT] = spare;
-    rc = h->step(cur, t, nxt, &acc, &r, &upd, tau);
-    if (rc) break;
-    t += r.tau_used;
-    if (results) results[k] = r;
-    s.steps += 1;
-    s.halvings += r.halvings;
-    s.radial_iterations += r.radial.iterations;
-    s.axial_iterations += r.axial.iterations;
-    s.cell_updates += upd;
-    s.cell_updates_accepted +=
-        static_cast<double>(h->active) * (r.radial.iterations + r.axial.iterations);
-    s.attempt_cells += 2.0 * static_cast<double>(h->active) * (r.halvings + 1);
-    double* accepted = const_cast<double*>(acc);
-    double* old = cur;
-    cur = accepted;
-    if (accepted == nxt) nxt = old; else spare = old;
-    // controller: carry the accepted tau, grow after `easy_steps` easy steps
-    tau = r.tau_used;
-    easy = r.halvings == 0 ? easy + 1 : 0;
-    if (easy >= easy_steps) {
-      tau = std::min(tau * grow, tau_max);
-      easy = 0;
-    }
-  }
-  h->buf[kField] = cur;
-  h->buf[kNext] = nxt;
-  h->buf[kIterT] = spare;
-  h->from_state(cur, field);
+  GrowthPlan plan{grow, tau_max, easy_steps, {tau, easy}};
+  h->to_state(field, h->buf[kField]);
+  rc = h->host_run(
+      &t, max_steps, plan,
+      [&](const pcgpu_step_result& r) { plan.update(plan.st, r.tau_used, r.halvings); },
+      [&](double tt) { return tt < t_end; }, results, &s);
+  h->from_state(h->buf[kField], field);
   CK(cudaStreamSynchronize(h->stream));
   GUARD_END(h)
   s.t_end = t;

@@ -322,6 +322,13 @@ class AdiStepper:
     def launch_count(self) -> int:
         return int(self._lib.pcgpu_launch_count(self._h))
 
+    def speculation_stats(self) -> dict:
+        """Host-driven runs (pcgpu_speculation_stats): speculative batches,
+        the steps they accepted, batches undone and replayed."""
+        b, s, r = C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(self._lib.pcgpu_speculation_stats(self._h, C.byref(b), C.byref(s), C.byref(r)))
+        return {"batches": b.value, "steps": s.value, "rollbacks": r.value}
+
     def resident_stats(self) -> dict:
         """The resident stepper (whole steps in one cooperative launch per
         batch; pcgpu_resident_stats): grid size (0: not used on this grid),

@@ -248,6 +248,45 @@ def test_resident_batches_and_host_redo_bitwise(cuda, monkeypatch):
     assert st2["host_steps"] == sum(1 for r in res if r.halvings > 0) > 0
 
 
+def test_speculative_batches_bitwise(cuda, monkeypatch):
+    """Host-driven runs (the configs[3] path) enqueue batches of steps with the
+    predicted Picard counts and read once per batch: configs[0]'s 2000 steps
+    mostly in batches, and a run whose counts change and that halves, where
+    batches are undone and replayed -- both bit for bit against the C
+    restatement, with the clamp counts; and the step-by-step path
+    (PCGPU_NO_SPECULATE) for comparison."""
+    monkeypatch.setenv("PCGPU_RESIDENT", "0")
+    case = configs.cfg0(2000)
+    g = case.grid()
+    port = PortStepper(case)
+    fo = make_field(g, case.solver.T0)
+    te_o, _, res_o = port.run(fo, 0.0, case.steps)
+    gpu = gpu_stepper(case, "exact")
+    fg = to_dev(make_field(g, case.solver.T0))
+    te_g, _, res_g = gpu.run(fg, 0.0, case.steps, keep_results=True)
+    assert te_g == te_o and np.array_equal(_seq(res_g), _seq(res_o))
+    assert np.array_equal(to_host(fg)[g.mask()], fo[g.mask()])
+    sp = gpu.speculation_stats()
+    assert sp["steps"] > case.steps // 2, sp
+    z = np.load(os.path.join(GOLD, "cfg0_coarse_halving.npz"))
+    name, build, init, steps, t0 = [c for c in _golden_cases() if c[0] == "cfg0_coarse_halving"][0]
+    for spec in (True, False):
+        if not spec:
+            monkeypatch.setenv("PCGPU_NO_SPECULATE", "1")
+        case2 = build()
+        gpu2 = gpu_stepper(case2, "exact")
+        f = to_dev(np.asfortranarray(z["initial"]))
+        t_end, _, res = gpu2.run(f, float(z["t0"]), int(z["steps"]), keep_results=True)
+        assert np.array_equal(_seq(res), z["seq"]) and t_end == float(z["t_end"])
+        assert np.array_equal(to_host(f)[case2.grid().mask()], z["final"][case2.grid().mask()])
+        assert gpu2.clamp_events() == [int(v) for v in z["clamp"]]
+        sp2 = gpu2.speculation_stats()
+        if spec:
+            assert sp2["batches"] > 0 and sp2["rollbacks"] > 0, sp2
+        else:
+            assert sp2["batches"] == 0
+
+
 def test_field_source_rejected_by_whole_steps(cuda):
     """A FIELD source's power is bound per half-step (the caller binds it
     before each half-step): step / run / evolve refuse it (ConfigError)
