@@ -51,56 +51,6 @@ void launch_axial_exact(const DevProblem& P, int it, double eps, double half_k, 
                         const double* ThN, const double* kbarN, const double* explN,
                         double* outN, double* wN, double* xN, DevStatus* st, cudaStream_t s);
 
-// ---- flow sweeps: Picard iterations first..last of one sweep in one launch ----
-// The lines of a sweep are independent across Picard iterations -- line l's
-// iteration it reads only line l's iterate, anchor and frozen terms -- and
-// only the stopping rule couples them (the max over all lines). So instead of
-// one launch per iteration, each ending in a tail where the SMs that had
-// fewer line blocks idle, a persistent cooperative grid takes (iteration,
-// line block) items from a ready queue in completion order: a block's next
-// iteration is queued when its current one ends, and any CTA takes it. An
-// item of iteration it runs iff no iteration before it converged or failed:
-// iterations <= it-2 are always known when it starts (the CTA waits for them:
-// depth-1 speculation), it-1 only when it > spec_limit (else the item runs on
-// the bet that it-1 does not converge; if it did, the item wrote the buffer of
-// it-2, which is dead then, and its status and clamp counters are its own
-// and discarded). The last CTA out merges the per-iteration statuses in the
-// reference's order (solver.cpp:243-256: an iteration's error, then its
-// convergence test) into the sweep's status and adds the clamp events of the
-// iterations that ran into DevProblem::clamp. Same kernels, same arithmetic:
-// bit-identical to the per-iteration launches.
-constexpr int kFlowMaxIt = 16;        // iterations per flow launch
-constexpr int kFlowMaxBlocks = 2048;  // line blocks (32 lines) per sweep
-struct FlowCtl {
-  unsigned int head, tail, finished, pad;
-  unsigned int done[kFlowMaxIt];             // line blocks finished, per iteration
-  int q[kFlowMaxIt * kFlowMaxBlocks];        // ready queue: item + 1 (0 = not yet pushed)
-  DevStatus st[kFlowMaxIt];                  // per iteration (delta at index it)
-  unsigned long long clamp[kFlowMaxIt][kMaxLayers];
-};
-// The sweep's arrays: iteration 1 reads src1 (the anchor copy), odd
-// iterations write `odd`, even ones `even` (each reads the other).
-struct FlowBufs {
-  const double* src1;
-  double* odd;
-  double* even;
-  const double *base, *ex, *aux;
-  double *w, *x;
-};
-// Whether a flow launch applies to a sweep of nlines lines (exact-x / exact-lean
-// lookups, TMA rows).
-// force: also when the lines fit one block per SM (tests).
-bool flow_applies(const DevProblem& P, bool axial, int nlines, bool force);
-// Enqueue iterations first..last (last - first < kFlowMaxIt) of a sweep whose
-// status is st (delta[first..last] and err merged into it). spec_limit: the
-// highest iteration that may start before its predecessor is known.
-void launch_radial_flow(const DevProblem& P, int first, int last, int spec_limit, double eps,
-                        double half_k, double pulse, const FlowBufs& B, DevStatus* st,
-                        FlowCtl* ctl, cudaStream_t s);
-void launch_axial_flow(const DevProblem& P, int first, int last, int spec_limit, double eps,
-                       double half_k, const FlowBufs& B, DevStatus* st, FlowCtl* ctl,
-                       cudaStream_t s);
-
 // ---- partitioned (multi-GPU) slabs, exact mode (adi_exact.cu) ----
 // z-slab: radial lines j0..j0+nj-1, T layout [i][j-j0] (ld nj);
 // r-slab: axial lines i0..i0+ni-1, N layout [j][i-i0] (ld ni).

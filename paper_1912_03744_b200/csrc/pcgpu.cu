@@ -234,8 +234,7 @@ struct pcgpu_stepper {
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
-  // tag: batch step + 1; last > 0: a flow launch covering iterations it..last
-  struct Timed { cudaEvent_t a, b; int sweep; int it; int tag; int last; };
+  struct Timed { cudaEvent_t a, b; int sweep; int it; int tag; };  // tag: batch step + 1
   std::vector<Timed> pending;
   double radial_ms = 0, axial_ms = 0;
   int64_t radial_launches = 0, axial_launches = 0;
@@ -392,11 +391,11 @@ struct pcgpu_stepper {
     (void)sweep;
     (void)it;
   }
-  void timed_end(int sweep, int it, cudaEvent_t a, int tag = 0, int last = 0) {
+  void timed_end(int sweep, int it, cudaEvent_t a, int tag = 0) {
     if (!timing) return;
     cudaEvent_t b = event();
     CK(cudaEventRecord(b, stream));
-    pending.push_back({a, b, sweep, it, tag, last});
+    pending.push_back({a, b, sweep, it, tag});
   }
   // After a sync: accumulate the durations of the iterations that ran (of
   // one sweep; tag < 0: every tag, else that batch step only).
@@ -408,10 +407,8 @@ struct pcgpu_stepper {
       if (t.it <= ran) {
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, t.a, t.b));
-        // a flow launch counts as the iterations of it that ran
-        const int n = t.last > 0 ? std::min(ran, t.last) - t.it + 1 : 1;
-        if (sweep == 0) { radial_ms += ms; radial_launches += n; }
-        else { axial_ms += ms; axial_launches += n; }
+        if (sweep == 0) { radial_ms += ms; ++radial_launches; }
+        else { axial_ms += ms; ++axial_launches; }
       }
     }
     pending.swap(keep);
@@ -422,39 +419,10 @@ struct pcgpu_stepper {
     ev_used = 0;
   }
 
-  // ---- flow sweeps (adi_kernels.h) --------------------------------------------
-  // flow_sweep[0] radial, [1] axial: set at create ($PCGPU_FLOW=0 off, =1 also
-  // on grids of one line block per SM; default: grids with more blocks than SMs)
-  bool flow_sweep[2] = {false, false};
-  FlowCtl* flow_ctl = nullptr;
-  bool flow_ready() {
-    if (flow_ctl) return true;
-    if (cudaMalloc(&flow_ctl, sizeof(FlowCtl)) != cudaSuccess) {
-      cudaGetLastError();
-      flow_ctl = nullptr;
-      flow_sweep[0] = flow_sweep[1] = false;
-      return false;
-    }
-    dev_allocs.push_back(flow_ctl);
-    return true;
-  }
-  FlowBufs radial_bufs() const {
-    const bool field = d.source_kind == PCGPU_SOURCE_FIELD;
-    return FlowBufs{buf[kTcT], buf[kHalfT], buf[kIterT], buf[kTcT], buf[kExpl],
-                    field ? buf[kPowT] : nullptr, buf[kW], buf[kX]};
-  }
-  FlowBufs axial_bufs(const double* anchor, const double* kbar, double* odd,
-                      double* even = nullptr) const {
-    return FlowBufs{anchor, odd, even ? even : buf[kIterT], anchor, buf[kExpl], kbar, buf[kW],
-                    buf[kX]};
-  }
-
   // ---- Picard loop driver shared by both sweeps ----------------------------
   // `launch(it)` enqueues iteration it; returns the converged iteration or 0.
-  // `range(first, last, spec_limit)` (flow sweeps, when flow_sweep[sweep]):
-  // iterations first..last in one launch instead.
-  template <typename Launch, typename Range>
-  int picard(int sweep, int& pred, Launch&& launch, Range&& range, pcgpu_outcome* o) {
+  template <typename Launch>
+  int picard(int sweep, int& pred, Launch&& launch, pcgpu_outcome* o) {
     const int max_iter = d.max_iter;
     int launched = 0;
     int batch = std::min(max_iter, std::max(1, pred) + 1);
@@ -463,22 +431,11 @@ struct pcgpu_stepper {
     o->last_delta = 0;
     while (launched < max_iter) {
       const int upto = std::min(max_iter, launched + batch);
-      if (flow_sweep[sweep] && flow_ready()) {
-        // the batch's last iteration starts only once its predecessor is known
-        for (int f = launched + 1; f <= upto; f += kFlowMaxIt) {
-          const int l = std::min(upto, f + kFlowMaxIt - 1);
-          cudaEvent_t a = nullptr;
-          timed_begin(sweep, f, &a);
-          range(f, l, upto - 1);
-          timed_end(sweep, f, a, 0, l);
-        }
-      } else {
-        for (int it = launched + 1; it <= upto; ++it) {
-          cudaEvent_t a = nullptr;
-          timed_begin(sweep, it, &a);
-          launch(it);
-          timed_end(sweep, it, a);
-        }
+      for (int it = launched + 1; it <= upto; ++it) {
+        cudaEvent_t a = nullptr;
+        timed_begin(sweep, it, &a);
+        launch(it);
+        timed_end(sweep, it, a);
       }
       launched = upto;
       fetch_status(launched);
@@ -522,9 +479,6 @@ struct pcgpu_stepper {
     const int conv = picard(0, pred_radial, [&](int it) {
       launch_radial_exact(P, it, d.epsilon, hk, pulse, src_of(it), buf[kTcT], buf[kExpl],
                           buf[kPowT], dst_of(it), buf[kW], buf[kX], st, stream);
-    }, [&](int first, int last, int spec) {
-      launch_radial_flow(P, first, last, spec, d.epsilon, hk, pulse, radial_bufs(), st, flow_ctl,
-                         stream);
     }, o);
     if (conv < 0) return -conv;
     if (conv > 0) *res = dst_of(conv);
@@ -554,7 +508,6 @@ struct pcgpu_stepper {
     for (auto& e : chunk_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     const size_t nst = static_cast<size_t>(kPipeMaxIter + 1) * kPipeChunks;
     CK(cudaMalloc(&st_pipe, sizeof(DevStatus) * nst));
-    CK(cudaMemset(st_pipe, 0, sizeof(DevStatus) * nst));  // DevStatus::clamp = nullptr
     dev_allocs.push_back(st_pipe);
     CK(cudaMallocHost(&st_pipe_host, sizeof(DevStatus) * nst));
     CK(cudaMalloc(&clamp_pipe, sizeof(unsigned long long) * (kPipeMaxIter + 1) * kMaxLayers));
@@ -697,9 +650,6 @@ struct pcgpu_stepper {
     const int conv = picard(1, pred_axial, [&](int it) {
       launch_axial_exact(P, it, d.epsilon, hk, src_of(it), anchor, kbar, buf[kExpl], dst_of(it),
                          buf[kW], buf[kX], st, stream);
-    }, [&](int first, int last, int spec) {
-      launch_axial_flow(P, first, last, spec, d.epsilon, hk, axial_bufs(anchor, kbar, out), st,
-                        flow_ctl, stream);
     }, o);
     if (conv < 0) return -conv;
     if (conv > 0) *res = dst_of(conv);
@@ -776,7 +726,6 @@ struct pcgpu_stepper {
     dev_allocs.push_back(res_log);
     CK(cudaMallocHost(&res_log_host, sizeof(ResLog) * kResBatch));
     CK(cudaMalloc(&res_st2, sizeof(DevStatus) * 2));
-    CK(cudaMemset(res_st2, 0, sizeof(DevStatus) * 2));
     dev_allocs.push_back(res_st2);
     CK(cudaMalloc(&res_probe_off, sizeof(int) * kResProbes));
     dev_allocs.push_back(res_probe_off);
@@ -999,7 +948,6 @@ struct pcgpu_stepper {
     }
     for (double* p : spec_n) dev_allocs.push_back(p);
     CK(cudaMalloc(&spec_st, sizeof(DevStatus) * 2 * kSpecBatch));
-    CK(cudaMemset(spec_st, 0, sizeof(DevStatus) * 2 * kSpecBatch));
     dev_allocs.push_back(spec_st);
     CK(cudaMallocHost(&spec_st_host, sizeof(DevStatus) * 2 * kSpecBatch));
     CK(cudaMalloc(&spec_clamp_save, sizeof(unsigned long long) * kMaxLayers));
@@ -1019,22 +967,14 @@ struct pcgpu_stepper {
     DevStatus* sa = sr + 1;
     const int nlater = 2 * (n - k);  // statuses after sr (sa included)
     launch_explicit_axial_exact(P, C, buf[kExpl], buf[kTcT], sr, stream, from);
-    if (flow_sweep[0] && flow_ready() && Lr <= kFlowMaxIt) {
+    for (int it = 1; it <= Lr; ++it) {
+      const double* src = it == 1 ? buf[kTcT] : (it % 2 == 0 ? buf[kHalfT] : buf[kIterT]);
+      double* dst = it % 2 == 1 ? buf[kHalfT] : buf[kIterT];
       cudaEvent_t a = nullptr;
-      timed_begin(0, 1, &a);
-      launch_radial_flow(P, 1, Lr, Lr - 1, d.epsilon, hk, pulse, radial_bufs(), sr, flow_ctl,
-                         stream);
-      timed_end(0, 1, a, k + 1, Lr);
-    } else {
-      for (int it = 1; it <= Lr; ++it) {
-        const double* src = it == 1 ? buf[kTcT] : (it % 2 == 0 ? buf[kHalfT] : buf[kIterT]);
-        double* dst = it % 2 == 1 ? buf[kHalfT] : buf[kIterT];
-        cudaEvent_t a = nullptr;
-        timed_begin(0, it, &a);
-        launch_radial_exact(P, it, d.epsilon, hk, pulse, src, buf[kTcT], buf[kExpl], buf[kPowT],
-                            dst, buf[kW], buf[kX], sr, stream);
-        timed_end(0, it, a, k + 1);
-      }
+      timed_begin(0, it, &a);
+      launch_radial_exact(P, it, d.epsilon, hk, pulse, src, buf[kTcT], buf[kExpl], buf[kPowT], dst,
+                          buf[kW], buf[kX], sr, stream);
+      timed_end(0, it, a, k + 1);
     }
     k_spec_verify<<<1, 32, 0, stream>>>(sr, Lr, d.epsilon, sa, nlater - 1, P.clamp,
                                         spec_clamp_save, d.n_layers, 0);
@@ -1047,22 +987,14 @@ struct pcgpu_stepper {
     double* anchor = buf[kTcT];  // halfN
     launch_axial_rhs_exact(P, hk, pulse, nullptr, buf[kPowN], kbar, buf[kExpl], anchor, sa, stream,
                            half);
-    if (flow_sweep[1] && flow_ready() && La <= kFlowMaxIt) {
+    for (int it = 1; it <= La; ++it) {
+      const double* src = it == 1 ? anchor : (it % 2 == 0 ? Po : Qo);
+      double* dst = it % 2 == 1 ? Po : Qo;
       cudaEvent_t a = nullptr;
-      timed_begin(1, 1, &a);
-      launch_axial_flow(P, 1, La, La - 1, d.epsilon, hk, axial_bufs(anchor, kbar, Po, Qo), sa,
-                        flow_ctl, stream);
-      timed_end(1, 1, a, k + 1, La);
-    } else {
-      for (int it = 1; it <= La; ++it) {
-        const double* src = it == 1 ? anchor : (it % 2 == 0 ? Po : Qo);
-        double* dst = it % 2 == 1 ? Po : Qo;
-        cudaEvent_t a = nullptr;
-        timed_begin(1, it, &a);
-        launch_axial_exact(P, it, d.epsilon, hk, src, anchor, kbar, buf[kExpl], dst, buf[kW],
-                           buf[kX], sa, stream);
-        timed_end(1, it, a, k + 1);
-      }
+      timed_begin(1, it, &a);
+      launch_axial_exact(P, it, d.epsilon, hk, src, anchor, kbar, buf[kExpl], dst, buf[kW],
+                         buf[kX], sa, stream);
+      timed_end(1, it, a, k + 1);
     }
     k_spec_verify<<<1, 32, 0, stream>>>(sa, La, d.epsilon, sa + 1, nlater - 2, P.clamp,
                                         spec_clamp_save, d.n_layers, 1);
@@ -1532,7 +1464,6 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
     h->d.row_extent = h->d.col_extent = nullptr;
 
     CK(cudaMalloc(&h->st, sizeof(DevStatus)));
-    CK(cudaMemset(h->st, 0, sizeof(DevStatus)));  // DevStatus::clamp = nullptr
     h->dev_allocs.push_back(h->st);
     CK(cudaMallocHost(&h->st_host, sizeof(DevStatus)));
 
@@ -1559,15 +1490,6 @@ int pcgpu_create(const pcgpu_desc* d, pcgpu_stepper** out) {
     const char* rv = std::getenv("PCGPU_RESIDENT");
     h->res_grid = (rv && std::atoi(rv) == 0) ? 0 : resident_grid(h->P);
     h->res_cluster = h->res_grid > 0 && resident_cluster(h->P, h->res_grid);
-    {  // flow sweeps for the host-driven path
-      const char* fv = std::getenv("PCGPU_FLOW");
-      const int mode = fv ? std::atoi(fv) : -1;  // 0 off, 1 forced, -1 auto
-      if (mode != 0) {
-        h->flow_sweep[0] = flow_applies(h->P, false, h->d.nz, mode == 1);
-        h->flow_sweep[1] = flow_applies(h->P, true, h->d.nr, mode == 1);
-        if (h->flow_sweep[0] || h->flow_sweep[1]) h->flow_ready();
-      }
-    }
     // the speculative batches' buffers up front (not inside a timed run)
     if (!h->res_grid && h->spec_ok()) h->spec_ready();  // outside any timed region
     h->launches0 = g_launches;
@@ -1647,10 +1569,6 @@ int32_t pcgpu_describe(const pcgpu_stepper* h, char* buf, int32_t len) {
   s += h->res_grid ? (std::string("resident:") + std::to_string(h->res_grid) +
                       (h->res_cluster ? "-cta-cluster" : "-cta-cooperative"))
                    : std::string("host-driven");
-  if (!h->res_grid && (h->flow_sweep[0] || h->flow_sweep[1])) {
-    s += " flow=";
-    s += h->flow_sweep[0] ? (h->flow_sweep[1] ? "radial+axial" : "radial") : "axial";
-  }
   if (buf && len > 0) {
     const size_t n = std::min(s.size(), static_cast<size_t>(len - 1));
     std::memcpy(buf, s.data(), n);

@@ -621,7 +621,6 @@ int pcgpu_dist_create(const pcgpu_desc* d, int32_t rank, int32_t nranks, const v
       R.recv = h->alloc(2 * std::max(zc, rc));  // sends go straight from the fields
       DevStatus* st = nullptr;
       DCK(cudaMalloc(&st, sizeof(DevStatus)));
-      DCK(cudaMemset(st, 0, sizeof(DevStatus)));  // DevStatus::clamp = nullptr
       h->allocs.push_back(st);
       R.st = st;
       sts.push_back(st);

@@ -20,13 +20,10 @@ def cuda():
     return torch.device("cuda:0")
 
 
-@pytest.fixture(params=["resident", "host", "flow"])
+@pytest.fixture(params=["resident", "host"])
 def stepper_path(request, monkeypatch):
     """Whole steps on the resident stepper (one cooperative launch per batch,
-    the default on grids of at most one line block per SM), host-driven with
-    one launch per Picard iteration, or host-driven with flow sweeps (every
-    Picard iteration of a sweep in one launch, the default on grids of more
-    line blocks than SMs; forced here on the small test grids)."""
+    the default on grids of at most one line block per SM) or host-driven
+    (one launch per Picard iteration, the large-grid path)."""
     monkeypatch.setenv("PCGPU_RESIDENT", "1" if request.param == "resident" else "0")
-    monkeypatch.setenv("PCGPU_FLOW", "1" if request.param == "flow" else "0")
     return request.param
