@@ -137,6 +137,10 @@ struct ResCtl {
   // count per phase -- 0 status reset, 1 K3, 2 radial iteration, 3 K4,
   // 4 axial iteration, 5 step epilogue
   unsigned long long prof_ns[8], prof_n[8];
+  // ... and per phase the busiest CTA's time from its exit of the previous
+  // barrier to its arrival at the next one (busy_max: the current phase)
+  unsigned long long prof_busy[8], busy_max[8];
+  unsigned long long prof_cyc;  // lead thread: clock64 over the profiled phases (SM clock)
 };
 struct ResArgs {
   double* X[3];  // N-layout field rotation: X[state] is the field

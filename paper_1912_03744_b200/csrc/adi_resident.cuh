@@ -68,13 +68,30 @@ __global__ void __launch_bounds__(kResThreads, 1)
   int hs = 0;  // half-step counter: status buffers alternate
   double(*te)[kT3Rows + 1] = reinterpret_cast<double(*)[kT3Rows + 1]>(sm);
   // phase profile (lead thread only)
-  unsigned long long t_last = 0;
+  unsigned long long t_last = 0, t_ph = 0;
+  long long c_last = 0;
   auto mark = [&](int phase) {
-    if (!A.profile || !lead) return;
-    const unsigned long long now = global_ns();
+    if (!A.profile) return;
+    if (tid == 0) t_ph = global_ns();  // this CTA's phase start
+    if (!lead) return;
+    const long long c_now = clock64();
+    A.ctl->prof_cyc += static_cast<unsigned long long>(c_now - c_last);
+    c_last = c_now;
+    const unsigned long long now = t_ph;
     A.ctl->prof_ns[phase] += now - t_last;
     A.ctl->prof_n[phase] += 1;
+    A.ctl->prof_busy[phase] += atomicExch(&A.ctl->busy_max[phase], 0ull);
     t_last = now;
+  };
+  // before a barrier: this CTA's busy time in the phase that ends there
+  auto busy = [&](int phase) {
+    if (A.profile && tid == 0) atomicMax(&A.ctl->busy_max[phase], global_ns() - t_ph);
+#ifdef PCGPU_TSPROF
+    if (tid == 0 && blockIdx.x < 64 && (phase == 2 || phase == 4)) {
+      g_rts[phase == 4][blockIdx.x][0] = t_ph;
+      g_rts[phase == 4][blockIdx.x][6] = global_ns();
+    }
+#endif
   };
   // Status of half-step hs is st2[hs & 1]. Both start reset; the buffer of
   // the next half-step is reset by the lead thread after the first grid
@@ -82,7 +99,10 @@ __global__ void __launch_bounds__(kResThreads, 1)
   if (lead) {
     reset_status(A.st2, max_iter);
     reset_status(A.st2 + 1, max_iter);
-    if (A.profile) t_last = global_ns();
+    if (A.profile) {
+      t_last = global_ns();
+      c_last = clock64();
+    }
   }
   grid.sync();
   mark(0);
@@ -118,6 +138,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
                                      bar_k34);
           bar_k34();
         }
+      busy(1);
       grid.sync();
       mark(1);
       if (lead) reset_status(st_next, max_iter);
@@ -136,6 +157,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
                                                      A.ExplT, nullptr, dst, A.W, A.Xs, st,
                                                      nullptr, vb);
         }
+        busy(2);
         grid.sync();
         mark(2);
         failed = ld_volatile_u64(&st->err) != kNoError;
@@ -173,6 +195,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
             bar_k34();
           }
         }
+        busy(3);
         grid.sync();
         mark(3);
         if (lead) reset_status(sa_next, max_iter);
@@ -191,6 +214,7 @@ __global__ void __launch_bounds__(kResThreads, 1)
                                                       A.ExplT, A.kbarN, dst, A.W, A.Xs, sa,
                                                       nullptr, vb);
           }
+          busy(4);
           grid.sync();
           mark(4);
           failed = ld_volatile_u64(&sa->err) != kNoError;

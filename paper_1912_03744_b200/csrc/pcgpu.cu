@@ -271,7 +271,7 @@ struct pcgpu_stepper {
   // $PCGPU_RES_PROF=1: per-phase device time of the resident batches,
   // printed to stderr when the stepper is destroyed
   bool res_profile = std::getenv("PCGPU_RES_PROF") != nullptr;
-  double res_prof_ns[8] = {}, res_prof_n[8] = {};
+  double res_prof_ns[8] = {}, res_prof_n[8] = {}, res_prof_busy[8] = {}, res_prof_cyc = 0;
   // the host functions behind the schedule (the reference's own through
   // pcgpu_set_host_clock, else the restatements below)
   pcgpu_clock_fn pulse_fn = nullptr, tau_fn = nullptr;
@@ -280,11 +280,15 @@ struct pcgpu_stepper {
   ~pcgpu_stepper() {
     if (res_profile && res_batches) {
       static const char* names[6] = {"start", "K3", "radial_it", "K4", "axial_it", "epilogue"};
-      std::fprintf(stderr, "pcgpu resident profile (%lld batches, %lld steps):",
-                   static_cast<long long>(res_batches), static_cast<long long>(res_steps));
+      double ns = 0;
+      for (int q = 1; q < 8; ++q) ns += res_prof_ns[q];
+      std::fprintf(stderr, "pcgpu resident profile (%lld batches, %lld steps, SM clock %.0f MHz):",
+                   static_cast<long long>(res_batches), static_cast<long long>(res_steps),
+                   ns > 0 ? res_prof_cyc / ns * 1e3 : 0.0);
       for (int q = 0; q < 6; ++q)
-        std::fprintf(stderr, " %s %.2f us x %.0f;", names[q],
-                     res_prof_n[q] ? res_prof_ns[q] / res_prof_n[q] / 1e3 : 0.0, res_prof_n[q]);
+        std::fprintf(stderr, " %s %.2f us (busiest CTA %.2f) x %.0f;", names[q],
+                     res_prof_n[q] ? res_prof_ns[q] / res_prof_n[q] / 1e3 : 0.0,
+                     res_prof_n[q] ? res_prof_busy[q] / res_prof_n[q] / 1e3 : 0.0, res_prof_n[q]);
       if (P.prof) {  // solver warp of line block 0: cycles per row waiting / in the chain
         unsigned long long c[16] = {};
         cudaMemcpy(c, P.prof, sizeof c, cudaMemcpyDeviceToHost);
@@ -775,6 +779,9 @@ struct pcgpu_stepper {
     if (res_profile) {
       CK(cudaMemsetAsync(res_ctl->prof_ns, 0, sizeof(res_ctl->prof_ns), stream));
       CK(cudaMemsetAsync(res_ctl->prof_n, 0, sizeof(res_ctl->prof_n), stream));
+      CK(cudaMemsetAsync(res_ctl->prof_busy, 0, sizeof(res_ctl->prof_busy), stream));
+      CK(cudaMemsetAsync(res_ctl->busy_max, 0, sizeof(res_ctl->busy_max), stream));
+      CK(cudaMemsetAsync(&res_ctl->prof_cyc, 0, sizeof(res_ctl->prof_cyc), stream));
     }
     launch_resident(P, A, res_grid, res_cluster, stream);
     CK(cudaMemcpyAsync(res_ctl_host, res_ctl, sizeof(ResCtl), cudaMemcpyDeviceToHost, stream));
@@ -785,7 +792,9 @@ struct pcgpu_stepper {
       for (int q = 0; q < 8; ++q) {
         res_prof_ns[q] += res_ctl_host->prof_ns[q];
         res_prof_n[q] += res_ctl_host->prof_n[q];
+        res_prof_busy[q] += res_ctl_host->prof_busy[q];
       }
+    if (res_profile) res_prof_cyc += static_cast<double>(res_ctl_host->prof_cyc);
     ++res_batches;
     res_steps += res_ctl_host->steps;
     return *res_ctl_host;
