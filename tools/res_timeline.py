@@ -1,4 +1,4 @@
-"""Per-CTA timeline of the resident stepper's last radial and axial Picard
+"""Per-CTA timeline (tile0: the solver starts the pivot chain) of the resident stepper's last radial and axial Picard
 phase on configs[0] (A/B build with -DPCGPU_TSPROF selected by PCGPU_LIB, run
 with PCGPU_RES_PROF=1): phase start -> line entry -> forward end -> bulk copy
 end -> back substitution end -> line end -> phase barrier, in microseconds."""
@@ -20,7 +20,7 @@ f = torch.full((g.nz(), g.nr()), c.solver.T0, dtype=torch.float64, device="cuda"
 s.run(f, 0.0, 20)
 torch.cuda.synchronize()
 lib = C.CDLL(_native.LIB_PATH)
-names = ["start", "entry", "fwd", "bulk", "back", "line", "barrier"]
+names = ["start", "entry", "fwd", "bulk", "back", "line", "barrier", "tile0"]
 for axial in (0, 1):
     buf = np.zeros((64, 8), dtype=np.uint64)
     assert lib.pcgpu_debug_rts(axial, buf.ctypes.data_as(C.c_void_p)) == 0
@@ -29,5 +29,5 @@ for axial in (0, 1):
     print("axial" if axial else "radial", "(us from the earliest phase start)")
     print("  cta " + " ".join(f"{n:>8}" for n in names))
     for r in rows:
-        vals = [(int(buf[r, k]) - t0) / 1e3 if buf[r, k] else float("nan") for k in range(7)]
+        vals = [(int(buf[r, k]) - t0) / 1e3 if buf[r, k] else float("nan") for k in range(8)]
         print(f"  {r:3d} " + " ".join(f"{v:8.2f}" for v in vals))
