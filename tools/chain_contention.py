@@ -34,6 +34,15 @@ for mode in (0, 1, 2, 3, 0):
     torch.cuda.synchronize()
     kt = s.kernel_timing()
     s.enable_kernel_timing(False)
+    for ax in (0, 1):
+        nb = 64
+        import numpy as np
+        w = np.zeros((nb, 2), dtype=np.uint64)
+        if lib.pcgpu_debug_fwait(ax, w.ctypes.data_as(C.c_void_p), nb) == 0:
+            m = w[:, 0] > 0
+            if m.any():
+                print(f"   {'axial' if ax else 'radial'} forward: work {w[m, 0].mean() / 1e3:.1f} us, "
+                      f"barrier waits {w[m, 1].mean() / 1e3:.1f} us (mean over CTAs)")
     print(f"{name} mode {mode}: radial {kt['radial_ms'] / max(kt['radial_launches'], 1) * 1e3:.1f} us "
           f"x {kt['radial_launches']}, axial {kt['axial_ms'] / max(kt['axial_launches'], 1) * 1e3:.1f} us "
           f"x {kt['axial_launches']}", flush=True)
