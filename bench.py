@@ -45,27 +45,62 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled during the timed region: NVML every
+    20 ms when pynvml can open the device, else nvidia-smi every 200 ms."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index, self.samples, self._stop = index, [], threading.Event()
+        self._nvml = self._open_nvml(index)
         self._t = threading.Thread(target=self._run, daemon=True)
+
+    @staticmethod
+    def _open_nvml(index):
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            try:
+                uuid = "GPU-" + str(torch.cuda.get_device_properties(index).uuid)
+                h = pynvml.nvmlDeviceGetHandleByUUID(uuid.encode())
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            bits = [pynvml.nvmlClocksEventReasonHwSlowdown,
+                    pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    pynvml.nvmlClocksEventReasonSwPowerCap]
+            return pynvml, h, float(mx), bits
+        except Exception:
+            return None
+
+    def _sample_nvml(self):
+        nv, h, mx, bits = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        self.samples.append([str(sm), str(mx), hex(r)] +
+                            ["Active" if r & b else "Not Active" for b in bits])
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
-                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                if self._nvml:
+                    self._sample_nvml()
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                          f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"],
+                                         capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.02 if self._nvml else 0.2)
 
     def __enter__(self):
         self._t.start()
@@ -80,12 +115,11 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4)
+        reasons = sorted({self.NAMES[k] for s in self.samples for k in range(4)
                           if len(s) > 3 + k and s[3 + k].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "samples": len(self.samples), "via": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def dist_env():
@@ -255,7 +289,13 @@ def main():
             tr = json.load(f).get(f"{args.config}:exact:{dom}")
         if tr:
             traffic = tr["dram_bytes_per_launch"] / 1e9
-            traffic_src = tr.get("source")
+            # Picard iteration 1 of every half-step attempt stages the anchor
+            # once (iterate == anchor) and moves fewer bytes: weight the
+            # per-launch traffic by the launches of each kind in the timed region
+            first = tr.get("dram_bytes_first_iteration")
+            n1 = stats["steps"] + stats["halvings"]
+            if first and dom_n >= n1 > 0:
+                traffic = (n1 * first / 1e9 + (dom_n - n1) * traffic) / dom_n
 
     # e2e through the reference-facing C-ABI with HOST buffers: pcgpu_step_host
     # copies the field H2D, steps, copies D2H every step.
@@ -362,7 +402,7 @@ def main():
                            controller=spec),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "traffic_unit": "GB per launch (ncu dram__bytes_read+write)",
+                         "traffic_unit": "GB per launch (ncu dram__bytes_read+write; mean over the timed launches)",
                          # the same launch time against the DRAM bytes it really moves
                          # (80 B per cell: the exact Thomas working set)
                          "traffic_frac": (traffic / (dom_ms / max(dom_n, 1) / 1e3) / peak
