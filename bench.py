@@ -122,6 +122,30 @@ class ClockSampler:
                 "samples": len(self.samples), "via": "nvml" if self._nvml else "nvidia-smi"}
 
 
+_REAL_STDOUT = None
+
+
+def claim_stdout():
+    """Keep stdout for the one JSON line: everything else written to fd 1 by
+    this process or its libraries (NCCL prints its version banner there)
+    goes to stderr."""
+    global _REAL_STDOUT
+    if _REAL_STDOUT is None:
+        sys.stdout.flush()
+        _REAL_STDOUT = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line):
+    data = (json.dumps(line) + "\n").encode()
+    if _REAL_STDOUT is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        sys.stdout.flush()
+        os.write(_REAL_STDOUT, data)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -194,6 +218,7 @@ def main():
                          "(under torchrun: a 1-rank NCCL communicator; validation of that path)")
     args = ap.parse_args()
     rank, world, local = dist_env()
+    claim_stdout()
 
     from paper_1912_03744_b200 import configs
     case = configs.CONFIGS[args.config]()
@@ -216,7 +241,7 @@ def main():
                 "cpu_baseline": r,
                 "e2e": {"value": r["value"], "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+        emit(line)
         return
 
     import numpy as np
@@ -415,7 +440,7 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "e2e_runner": e2e_runner, "clocks": clk.summary(),
             "gpu_launches": launches, "supplementary": supp,
         }
-        print(json.dumps(line))
+        emit(line)
     if pg:
         pg.destroy_process_group()
 
@@ -526,7 +551,7 @@ def run_partitioned(args, case, rank, world, local, pg, grid_desc, metric):
                               4 * 8 * g.nr() * g.nz() // world * (world - 1) // world},
             "roofline": roofline, "clocks": clk.summary(), "gpu_launches": launches, "e2e": e2e,
         }
-        print(json.dumps(line))
+        emit(line)
 
 
 def gpu_stepper_for(case, device):
