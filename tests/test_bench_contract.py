@@ -26,3 +26,22 @@ def test_reference_arm_json_line():
     assert cb["value"] == d["value"] and cb["kind"] in ("reference", "port") and cb["cores"] >= 1
     assert d["e2e"] == {"value": d["value"], "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
+
+
+def test_stdout_is_only_the_json_line():
+    """Whatever this process or its libraries write to fd 1 (NCCL prints its
+    version banner there) goes to stderr; stdout holds the one JSON line."""
+    code = (
+        "import os, sys, json\n"
+        "sys.path.insert(0, %r)\n"
+        "import bench\n"
+        "bench.claim_stdout()\n"
+        "os.write(1, b'NCCL version 2.28.9+cuda12.9\\n')\n"   # a C library writing to fd 1
+        "print('a python print')\n"
+        "bench.emit({'metric': 'm', 'value': 1.0})\n"
+    ) % ROOT
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.splitlines() == [json.dumps({"metric": "m", "value": 1.0})]
+    assert "NCCL version" in r.stderr and "a python print" in r.stderr
